@@ -1,0 +1,383 @@
+#!/usr/bin/env python
+"""bench.py -- APBF simulation-step throughput on B200 (BASELINE.json metric).
+
+A "step" is one Solver::stepFrame (solver.hpp:228-233) = LOD assignment +
+`substeps` substeps + the end-of-frame density metrics, over the C3 workload
+(BASELINE.json configs[2]): the 1M-particle ocean layer, APBF {5..10} with
+camera-distance LOD (scenarios/ocean_1m.cfg, SplitMix64 seed 1 -- the
+reference's own spawner, restated in paper_1608_04721_b200/scenario.py).
+
+value  = particle-iterations/s (FrameStats.totalIterations summed over the K
+         timed frames / device time of those frames, CUDA events recorded on
+         the solver's own launching stream), state resident in HBM.
+e2e    = the same metric through the reference-facing call with HOST buffers:
+         every step uploads the ParticleSet from pinned host memory
+         (apbf_gpu_set_state), steps, and downloads it (apbf_gpu_get_state).
+--impl reference = the reference's own CPU implementation (oracle/_ref:
+         Solver<double> compiled from /root/reference, OpenMP over all host
+         cores) on the same workload.
+
+Usage: python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+N > 1 is launched by torchrun; every rank simulates its own 1M tank (weak
+scaling, independent tanks -- the z-slab decomposition is the next row).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "sim steps/sec & particle-iterations/sec at 1M particles, 1/2/4/8 B200"
+UNIT = "particle-iterations/s"
+# Algorithmic bytes per particle-iteration (FP32 logical sizes):
+# lambda pass reads x*_i 12 + m_i 4 + w_i 4, writes lambda_i 4; the delta-p +
+# apply pass reads x*_i 12 + lambda_i 4 + w_i 4 and writes x*_i 12.
+BYTES_PER_PI = {"lambda": 24, "deltap_apply": 32}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--scenario", default="ocean_1m")
+    ap.add_argument("--seed", type=int, default=1)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--cpu-frames", type=int, default=1, help="timed reference frames (cpu_baseline)")
+    return ap.parse_args()
+
+
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.path = None
+
+    def start(self):
+        fd, self.path = tempfile.mkstemp(suffix=".csv")
+        os.close(fd)
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            t = [x.strip() for x in line.split(",")]
+            if len(t) < 9:
+                continue
+            try:
+                sm.append(float(t[1]))
+                mx.append(float(t[2]))
+            except ValueError:
+                continue
+            for k, v in zip(names, t[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(k)
+        os.unlink(self.path)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def ncu_traffic(kernel: str):
+    """Per-launch DRAM bytes of `kernel` from the committed ncu --set full
+    summary (profiles/ncu_summary.json), or None."""
+    path = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        return d["kernels"][kernel]["dram_bytes_per_launch"]
+    except Exception:
+        return None
+
+
+def cpu_reference_sample(spec, seed, frames):
+    """The reference CPU implementation on a bounded sample of the workload:
+    `frames` full stepFrame calls of the same scenario (after one warm-up
+    frame), Solver<double> over all host cores (deterministic=false)."""
+    import numpy as np
+
+    from oracle import oracle as O
+    from paper_1608_04721_b200 import scenario as S
+    if O.ref_available():
+        pos = S.spawn_scenario(spec, seed)
+        n = pos.shape[0]
+        mass = S.scenario_mass(spec)
+        st = O.RefState(pos, pos, np.zeros_like(pos), np.full(n, mass), np.full(n, 1.0 / mass),
+                        np.zeros(n), np.full(n, spec.solver.range.n_max, np.int32))
+        cfg = spec.solver
+        cfg.deterministic = False
+        sv = O.RefSolver(cfg, spec.scene, prec=8)
+        kind, cores = "reference", int(O.rlib().ref_omp_threads())
+    else:
+        st = S.make_state(spec, seed)
+        sv = O.OracleSolver(spec.solver, spec.scene)
+        kind, cores = "port", 1
+    sv.step_frame(st, spec.camera, spec.lod, 0)
+    t0 = time.perf_counter()
+    its = 0
+    for f in range(frames):
+        its += sv.step_frame(st, spec.camera, spec.lod, 1 + f).total_iterations
+    dt = time.perf_counter() - t0
+    return {"value": its / dt, "unit": UNIT, "cores": cores, "kind": kind,
+            "sample": f"{frames} full stepFrame(s) of {spec.name} ({spec.particle_count()} particles, "
+                      f"APBF {{{spec.solver.range.n_min}..{spec.solver.range.n_max}}}) after 1 warm-up "
+                      f"frame; {'Solver<double> from /root/reference via oracle/_ref' if kind == 'reference' else 'C oracle port'}",
+            "seconds_per_step": dt / frames}
+
+
+def dist_setup(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    pg = None
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        pg = dist
+    return world, rank, local, pg
+
+
+def barrier(pg):
+    if pg is not None:
+        pg.barrier()
+
+
+def allreduce_max(pg, v: float) -> float:
+    if pg is None:
+        return v
+    import torch
+    t = torch.tensor([v], dtype=torch.float64, device="cuda")
+    pg.all_reduce(t, op=pg.ReduceOp.MAX)
+    return float(t.item())
+
+
+def allreduce_sum(pg, v: float) -> float:
+    if pg is None:
+        return v
+    import torch
+    t = torch.tensor([v], dtype=torch.float64, device="cuda")
+    pg.all_reduce(t, op=pg.ReduceOp.SUM)
+    return float(t.item())
+
+
+def run_reference(args, world, rank):
+    if rank != 0:
+        return 0
+    from paper_1608_04721_b200 import scenario as S
+    spec = S.build_scenario(args.scenario)
+    # bounded: each step is one full frame of the 1M workload on the CPU
+    steps = max(1, min(args.steps, 5))
+    res = cpu_reference_sample(spec, args.seed, steps)
+    line = {"metric": METRIC, "value": res["value"], "unit": UNIT, "n_gpus": args.gpus,
+            "steps": steps, "warmup": 1, "ms_per_step": res["seconds_per_step"] * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "impl": "reference",
+            "config": {"workload": f"{spec.name}: {spec.particle_count()} particles, APBF "
+                                   f"{spec.solver.range.n_min}..{spec.solver.range.n_max}, "
+                                   f"lod={spec.lod.model.name.lower()}, rank 0 only",
+                       "scenario_file": f"scenarios/{args.scenario}.cfg", "seed": args.seed},
+            "cpu_baseline": {k: res[k] for k in ("value", "unit", "cores", "kind", "sample")},
+            "e2e": {"value": res["value"], "unit": UNIT, "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def run_ours(args, world, rank, local, pg):
+    import ctypes as C
+
+    import numpy as np
+    import torch
+
+    from paper_1608_04721_b200 import Solver
+    from paper_1608_04721_b200 import scenario as S
+
+    spec = S.build_scenario(args.scenario)
+    n = spec.particle_count()
+    solver = Solver(spec.solver, spec.scene, device=local)
+    state = S.make_state(spec, args.seed + rank)
+    solver.upload(state)
+    cam, lod = spec.camera, spec.lod
+    torch.cuda.set_device(local)
+    ext = torch.cuda.ExternalStream(solver.stream_handle(), device=local)
+
+    for f in range(max(3, args.warmup)):
+        solver.step_frame_resident(cam, lod, f)
+
+    # ---------------- device-resident timed region ----------------
+    solver.set_kernel_timing(True)
+    launches0 = Solver.launch_count()
+    clocks = ClockSampler(local)
+    clocks.start()
+    barrier(pg)
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(ext)
+    its = 0
+    for f in range(args.steps):
+        its += solver.step_frame_resident(cam, lod, 1000 + f).total_iterations
+    e1.record(ext)
+    e1.synchronize()
+    torch.cuda.synchronize()
+    barrier(pg)
+    clk = clocks.stop()
+    launches = Solver.launch_count() - launches0
+    ms = e0.elapsed_time(e1)
+    kt = solver.kernel_times()
+    solver.set_kernel_timing(False)
+    entries, _ = solver.last_neighbor_stats()
+
+    ms_max = allreduce_max(pg, ms)
+    its_all = allreduce_sum(pg, float(its))
+    value = its_all / (ms_max / 1e3)
+
+    # ---------------- e2e through the C-ABI with host buffers ----------------
+    e2e = None
+    if not args.no_e2e:
+        host = S.make_state(spec, args.seed + rank)
+        pinned = {}
+        for k in ("x", "x_star", "v", "mass", "inv_mass", "lambda_", "level"):
+            a = getattr(host, k)
+            t = torch.empty(a.shape, dtype=torch.from_numpy(a).dtype, pin_memory=True)
+            t.numpy()[...] = a
+            pinned[k] = t
+            setattr(host, k, t.numpy())
+        solver.upload(host)
+        for f in range(2):
+            solver.step_frame(host, cam, lod, f)
+        barrier(pg)
+        torch.cuda.synchronize()
+        e2 = torch.cuda.Event(enable_timing=True)
+        e3 = torch.cuda.Event(enable_timing=True)
+        e2.record(ext)
+        its2 = 0
+        for f in range(args.steps):
+            its2 += solver.step_frame(host, cam, lod, 2000 + f).total_iterations
+        e3.record(ext)
+        e3.synchronize()
+        barrier(pg)
+        ms2 = allreduce_max(pg, e2.elapsed_time(e3))
+        its2_all = allreduce_sum(pg, float(its2))
+        words = 13  # x3 + x*3 + v3 + m + w + lambda + level
+        e2e = {"value": its2_all / (ms2 / 1e3), "unit": UNIT,
+               "h2d_bytes_per_step": 4 * words * n, "d2h_bytes_per_step": 4 * words * n,
+               "ms_per_step": ms2 / args.steps,
+               "note": "per step: apbf_gpu_set_state from pinned host arrays + step_frame + "
+                       "apbf_gpu_get_state into them (the reference's stepFrame(ParticleSet&) contract)"}
+
+    if rank != 0:
+        return 0
+
+    hbm_peak, peak_kind = peaks()
+    dom = "deltap_apply" if kt["deltap_ms"] >= kt["lambda_ms"] else "lambda"
+    dom_ms = kt["deltap_ms"] if dom == "deltap_apply" else kt["lambda_ms"]
+    per_launch_ms = dom_ms / max(1, kt["launches"])
+    pis_per_launch = kt["particle_iterations"] / max(1, kt["launches"])
+    alg_bytes = BYTES_PER_PI[dom] * pis_per_launch
+    achieved = alg_bytes / (per_launch_ms / 1e3) / 1e9
+    nbar = entries / n
+    # flops per particle-iteration from the reference expressions (SURVEY.md
+    # 8d): lambda 37 per non-self pair + 31, delta-p+apply 23 per pair + 4 (+3)
+    flops_pi = {"lambda": 37 * (nbar - 1) + 31, "deltap_apply": 23 * (nbar - 1) + 7}[dom]
+    sm_mhz = clk.get("sm_mhz") or 1965.0
+    fp32_peak = 148 * 128 * sm_mhz * 1e6 / 1e12  # non-FMA TFLOP/s (parity build, -fmad=false)
+    fp32_achieved = flops_pi * pis_per_launch / (per_launch_ms / 1e3) / 1e12
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": max(3, args.warmup), "ms_per_step": ms_max / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic",
+        "config": {"workload": f"{spec.name}: {n} particles/GPU, APBF "
+                               f"{spec.solver.range.n_min}..{spec.solver.range.n_max}, "
+                               f"lod={spec.lod.model.name.lower()}, {spec.solver.substeps} substeps, "
+                               "metrics pass included",
+                   "scenario_file": f"scenarios/{args.scenario}.cfg", "seed": args.seed,
+                   "parallelism": f"{world} independent tanks (one per GPU)",
+                   "l2": "inputs larger than L2 (~0.5 GB device state + scratch per frame)"},
+        "steps_per_s": args.steps / (ms_max / 1e3),
+        "particle_iterations_per_step": its_all / args.steps,
+        "e2e": e2e,
+        "gpu_launches": launches,
+        "clocks": clk,
+        "roofline": {"bound": "hbm", "kernel": f"k_{dom}", "achieved": achieved,
+                     "peak": hbm_peak, "unit": "GB/s", "frac": achieved / hbm_peak,
+                     "peak_source": peak_kind, "traffic": ncu_traffic(f"k_{dom}"),
+                     "algorithmic_bytes_per_launch": alg_bytes,
+                     "avg_launch_ms": per_launch_ms, "launches": kt["launches"],
+                     "share_of_step": (kt["lambda_ms"] + kt["deltap_ms"]) / ms,
+                     "note": "FP32-issue-bound gather kernel; HBM fraction low by construction "
+                             "(SURVEY.md 8d), see roofline_fp32"},
+        "roofline_fp32": {"bound": "fp32", "achieved": fp32_achieved, "peak": fp32_peak,
+                          "unit": "TFLOP/s", "frac": fp32_achieved / fp32_peak,
+                          "nbar": nbar, "flops_per_particle_iteration": flops_pi,
+                          "peak_note": "148 SMs x 128 lanes x median SM clock, no FMA credit"},
+        "kernel_ms": {"lambda_total": kt["lambda_ms"], "deltap_apply_total": kt["deltap_ms"],
+                      "timed_region_total": ms},
+    }
+    if world == 1 and not args.no_cpu_baseline:
+        res = cpu_reference_sample(S.build_scenario(args.scenario), args.seed, args.cpu_frames)
+        line["cpu_baseline"] = {k: res[k] for k in ("value", "unit", "cores", "kind", "sample")}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    args = parse()
+    world, rank, local, pg = dist_setup(args) if args.impl == "ours" else (
+        int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("RANK", "0")), 0, None)
+    try:
+        if args.impl == "reference":
+            return run_reference(args, world, rank)
+        return run_ours(args, world, rank, local, pg)
+    finally:
+        if pg is not None:
+            pg.destroy_process_group()
+
+
+if __name__ == "__main__":
+    sys.exit(main())

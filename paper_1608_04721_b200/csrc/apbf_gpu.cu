@@ -1,0 +1,1073 @@
+// apbf_gpu.cu -- host side of the B200 APBF step behind the C-ABI in
+// include/apbf_gpu.h.  One solver handle = one device, one stream, device-
+// resident ParticleSet.  See DESIGN.md for the pipeline and data layout.
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <stdexcept>
+#include <string>
+#include <vector>
+#include <array>
+
+#include "apbf_kernels.cuh"
+
+using namespace apbf_gpu;
+
+namespace {
+
+// ------------------------------------------------------------- errors
+
+struct ApiError {
+    int code;
+    std::string pass;
+    int particle;
+    std::string msg;
+};
+
+[[noreturn]] void fail(int code, const std::string& msg) { throw ApiError{code, "", -1, msg}; }
+
+[[noreturn]] void numerical(const std::string& pass, int particle, const std::string& detail) {
+    throw ApiError{APBF_ERR_NUMERICAL, pass, particle,
+                   "numerical abort in pass '" + pass + "' at particle " + std::to_string(particle) +
+                       ": " + detail};
+}
+
+#define CK(x)                                                                                 \
+    do {                                                                                      \
+        cudaError_t e_ = (x);                                                                 \
+        if (e_ != cudaSuccess)                                                                \
+            throw ApiError{APBF_ERR_CUDA, "", -1,                                             \
+                           std::string(#x) + ": " + cudaGetErrorString(e_) + " at " +         \
+                               __FILE__ + ":" + std::to_string(__LINE__)};                    \
+    } while (0)
+
+#define LAUNCH_CHECK() CK(cudaGetLastError())
+
+// Counts every kernel this library launches (bench.py reports it).
+static unsigned long long g_launches = 0;
+#define KL(...)          \
+    do {                 \
+        __VA_ARGS__;     \
+        ++g_launches;    \
+    } while (0)
+
+int32_t to_err(const ApiError& e, apbf_error* out) {
+    if (out) {
+        out->code = e.code;
+        out->particle = e.particle;
+        std::snprintf(out->pass, sizeof out->pass, "%s", e.pass.c_str());
+        std::snprintf(out->message, sizeof out->message, "%s", e.msg.c_str());
+    }
+    return e.code;
+}
+
+template <class F>
+int32_t guarded(apbf_error* err, F&& f) {
+    if (err) std::memset(err, 0, sizeof *err);
+    try {
+        f();
+        return APBF_OK;
+    } catch (const ApiError& e) {
+        return to_err(e, err);
+    } catch (const std::bad_alloc&) {
+        return to_err(ApiError{APBF_ERR_RUNTIME, "", -1, "host allocation failed"}, err);
+    } catch (const std::exception& e) {
+        return to_err(ApiError{APBF_ERR_RUNTIME, "", -1, e.what()}, err);
+    }
+}
+
+inline int blocks(long long n, int t) { return (int)std::max<long long>(1, (n + t - 1) / t); }
+
+// ------------------------------------------------------------- buffers
+
+template <class T>
+struct DBuf {
+    T* p = nullptr;
+    size_t n = 0;
+    DBuf() = default;
+    DBuf(const DBuf&) = delete;
+    DBuf& operator=(const DBuf&) = delete;
+    ~DBuf() { release(); }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        n = 0;
+    }
+    void ensure(size_t m) {
+        if (m <= n && p) return;
+        release();
+        CK(cudaMalloc(&p, sizeof(T) * std::max<size_t>(m, 1)));
+        n = std::max<size_t>(m, 1);
+    }
+};
+
+struct SetBufs {
+    DBuf<float4> X, V, XS;
+    DBuf<float> W, L;
+    DBuf<int> LV;
+    void ensure(size_t n) {
+        X.ensure(n);
+        V.ensure(n);
+        XS.ensure(n);
+        W.ensure(n);
+        L.ensure(n);
+        LV.ensure(n);
+    }
+    StateSet view() { return StateSet{X.p, V.p, XS.p, W.p, L.p, LV.p}; }
+};
+
+// Device scratch shared by the solver and the component entry points.
+struct Workspace {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    DBuf<Ctl> ctl;
+    Ctl* h_ctl = nullptr;  // pinned mirror
+    DBuf<int> cellCount;   // kMaxCells + 1 (cellStart after the scan)
+    DBuf<int> partial;
+    DBuf<int> key, slot, bucket, perm;
+    DBuf<Scene> scene;
+    DBuf<RadixSel> rs;
+    DBuf<int> depth;
+    DBuf<float> dist;
+    DBuf<unsigned> keys;
+    DBuf<float4> tmp4;
+
+    explicit Workspace(int dev) : device(dev) {
+        CK(cudaSetDevice(dev));
+        CK(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+        ctl.ensure(1);
+        CK(cudaMallocHost(&h_ctl, sizeof(Ctl)));
+        partial.ensure(kScanGrid);
+        scene.ensure(1);
+        rs.ensure(1);
+    }
+    ~Workspace() {
+        if (h_ctl) cudaFreeHost(h_ctl);
+        if (stream) cudaStreamDestroy(stream);
+    }
+    void ensure_particles(size_t n) {
+        key.ensure(n);
+        slot.ensure(n);
+        bucket.ensure(n);
+        perm.ensure(n);
+    }
+    void ensure_cells() { cellCount.ensure((size_t)kMaxCells + 1); }
+
+    // UniformGrid::build on float4 positions P (AABB already in grid g):
+    // params, histogram, scan, stable counting sort -> perm, cellStart.
+    void run_grid(int g, const float4* P, int n, float h, float pad, bool contacts, float radius) {
+        ensure_cells();
+        ensure_particles(n);
+        KL(k_grid_params<<<1, 1, 0, stream>>>(ctl.p, g, h, pad));
+        KL(k_zero_cells<<<4 * 148, 256, 0, stream>>>(ctl.p, g, cellCount.p));
+        KL(k_cell_keys<<<blocks(n, 256), 256, 0, stream>>>(n, P, ctl.p, g, h, cellCount.p, key.p, slot.p,
+                                                        scene.p, radius, contacts ? 1 : 0));
+        KL(k_scan_reduce<<<kScanGrid, kScanBlock, 0, stream>>>(ctl.p, g, cellCount.p, partial.p));
+        KL(k_scan_partials<<<1, kScanBlock, 0, stream>>>(ctl.p, partial.p, kScanGrid));
+        KL(k_scan_apply<<<kScanGrid, kScanBlock, 0, stream>>>(ctl.p, g, cellCount.p, partial.p));
+        KL(k_bucket_fill<<<blocks(n, 256), 256, 0, stream>>>(n, ctl.p, key.p, slot.p, cellCount.p,
+                                                          bucket.p));
+        KL(k_stable_rank<<<blocks(n, 256), 256, 0, stream>>>(n, ctl.p, key.p, cellCount.p, bucket.p,
+                                                          perm.p));
+        LAUNCH_CHECK();
+    }
+
+    void read_ctl() {
+        CK(cudaMemcpyAsync(h_ctl, ctl.p, sizeof(Ctl), cudaMemcpyDeviceToHost, stream));
+        CK(cudaStreamSynchronize(stream));
+    }
+};
+
+// ------------------------------------------------------- host helpers
+
+bool finite3h(const float* p) { return std::isfinite(p[0]) && std::isfinite(p[1]) && std::isfinite(p[2]); }
+
+// SdfScene from the C-ABI primitives, with the reference constructors'
+// validation and the half-space normalisation in float (sdf.hpp:23-73).
+Scene make_scene(const apbf_sdf_primitive* prims, int n, float step) {
+    if (n < 0) fail(APBF_ERR_INVALID_ARGUMENT, "negative primitive count");
+    if (n > kMaxPrims) fail(APBF_ERR_INVALID_ARGUMENT, "too many SDF primitives for the GPU scene");
+    Scene sc;
+    std::memset(&sc, 0, sizeof sc);
+    sc.n = n;
+    sc.step = step;
+    for (int k = 0; k < n; ++k) {
+        apbf_sdf_primitive p = prims[k];
+        switch (p.kind) {
+            case APBF_SDF_HALF_SPACE: {
+                const float len = std::sqrt(sqn3(p.p[0], p.p[1], p.p[2]));
+                if (!(len > 0.0f)) fail(APBF_ERR_INVALID_ARGUMENT, "half-space normal must be nonzero");
+                p.p[0] /= len;
+                p.p[1] /= len;
+                p.p[2] /= len;
+                break;
+            }
+            case APBF_SDF_SPHERE:
+                if (!(p.a > 0.0f)) fail(APBF_ERR_INVALID_ARGUMENT, "sphere radius must be positive");
+                break;
+            case APBF_SDF_BOX:
+                if (!(min_std(p.q[0], min_std(p.q[1], p.q[2])) > 0.0f))
+                    fail(APBF_ERR_INVALID_ARGUMENT, "box half extents must be positive");
+                break;
+            case APBF_SDF_CONE:
+                if (!(p.a > 0.0f) || !(p.b > 0.0f))
+                    fail(APBF_ERR_INVALID_ARGUMENT, "cone radius and height must be positive");
+                break;
+            default:
+                fail(APBF_ERR_INVALID_ARGUMENT, "unknown primitive kind");
+        }
+        sc.prim[k] = p;
+    }
+    return sc;
+}
+
+// CameraFrame (depth_splat.hpp:29-71) on the host, in float.
+CamFrame make_frame(const apbf_camera& cam) {
+    if (cam.width <= 0 || cam.height <= 0)
+        fail(APBF_ERR_INVALID_ARGUMENT, "camera resolution must be positive in both axes");
+    float d[3] = {cam.look_at[0] - cam.eye[0], cam.look_at[1] - cam.eye[1], cam.look_at[2] - cam.eye[2]};
+    if (!(sqn3(d[0], d[1], d[2]) > 0.0f))
+        fail(APBF_ERR_INVALID_ARGUMENT, "camera look-at must differ from eye");
+    if (!(cam.vertical_fov > 0.0f) || !(cam.vertical_fov < kPi))
+        fail(APBF_ERR_INVALID_ARGUMENT, "vertical fov must lie in (0, pi)");
+    if (!(cam.near_clip > 0.0f)) fail(APBF_ERR_INVALID_ARGUMENT, "near clip must be positive");
+    CamFrame f;
+    const float z = sqn3(d[0], d[1], d[2]);
+    if (z > 0.0f) {
+        const float s = std::sqrt(z);
+        d[0] /= s;
+        d[1] /= s;
+        d[2] /= s;
+    }
+    for (int a = 0; a < 3; ++a) {
+        f.eye[a] = cam.eye[a];
+        f.forward[a] = d[a];
+    }
+    const float* u = cam.up;
+    f.right[0] = f.forward[1] * u[2] - f.forward[2] * u[1];
+    f.right[1] = f.forward[2] * u[0] - f.forward[0] * u[2];
+    f.right[2] = f.forward[0] * u[1] - f.forward[1] * u[0];
+    const float len = std::sqrt(sqn3(f.right[0], f.right[1], f.right[2]));
+    if (!(len > 1e-12f)) fail(APBF_ERR_INVALID_ARGUMENT, "camera up is parallel to the view direction");
+    for (int a = 0; a < 3; ++a) f.right[a] /= len;
+    f.trueUp[0] = f.right[1] * f.forward[2] - f.right[2] * f.forward[1];
+    f.trueUp[1] = f.right[2] * f.forward[0] - f.right[0] * f.forward[2];
+    f.trueUp[2] = f.right[0] * f.forward[1] - f.right[1] * f.forward[0];
+    f.tanY = std::tan(cam.vertical_fov / 2.0f);
+    f.tanX = f.tanY * (float)cam.width / (float)cam.height;
+    f.width = cam.width;
+    f.height = cam.height;
+    f.nearClip = cam.near_clip;
+    return f;
+}
+
+void validate_lod(const apbf_lod_config& l) {
+    if (!l.auto_range && !(l.d_min < l.d_max))
+        fail(APBF_ERR_INVALID_ARGUMENT, "lod distance range requires d_min < d_max");
+}
+
+// LOD on device for positions X (float4): levels into LV.
+// lodDtc (lod.hpp:83-104) / lodDtvs (lod.hpp:109-156).
+void run_lod(Workspace& ws, const float4* X, int n, const apbf_camera& cam, const apbf_lod_config& lod,
+             float radius, int* LV) {
+    cudaStream_t st = ws.stream;
+    ws.dist.ensure(n);
+    ws.keys.ensure(n);
+    const bool dtvs = lod.model == APBF_LOD_DTVS;
+    if (dtvs) {
+        const CamFrame f = make_frame(cam);
+        const size_t px = (size_t)cam.width * cam.height;
+        ws.depth.ensure(px);
+        KL(k_fill_int<<<blocks((long long)px, 256), 256, 0, st>>>(ws.depth.p, (int)px, 0x7f800000));
+        KL(k_splat<<<blocks(n, 256), 256, 0, st>>>(n, X, radius, f, ws.depth.p));
+        KL(k_dtvs_gap<<<blocks(n, 256), 256, 0, st>>>(n, X, radius, f, ws.depth.p, ws.dist.p, ws.keys.p,
+                                                   ws.ctl.p));
+    } else {
+        KL(k_dtc_dist<<<blocks(n, 256), 256, 0, st>>>(n, X, cam.eye[0], cam.eye[1], cam.eye[2], ws.dist.p,
+                                                   ws.keys.p));
+    }
+    if (lod.auto_range) {
+        KL(k_rs_init<<<1, 1, 0, st>>>(ws.rs.p, ws.ctl.p, n, dtvs ? 1 : 0));
+        KL(k_rs_clear<<<1, 1024, 0, st>>>(ws.rs.p));
+        const int hb = std::min(blocks(n, 256), 2 * 148);
+        for (int pass = 0; pass < 3; ++pass) {
+            KL(k_rs_hist<<<hb, 256, 0, st>>>(n, ws.keys.p, ws.rs.p, pass));
+            KL(k_rs_select<<<1, 1024, 0, st>>>(ws.rs.p, pass));
+        }
+    }
+    KL(k_lod_params<<<1, 1, 0, st>>>(ws.rs.p, ws.ctl.p, lod.auto_range, lod.d_min, lod.d_max, dtvs ? 1 : 0));
+    KL(k_lod_map<<<blocks(n, 256), 256, 0, st>>>(n, ws.ctl.p, ws.dist.p, ws.keys.p, dtvs ? 1 : 0, lod.n_min,
+                                              lod.n_max, LV));
+    LAUNCH_CHECK();
+}
+
+std::vector<Workspace*>& global_workspaces() {
+    static std::vector<Workspace*> w;
+    return w;
+}
+
+Workspace& component_ws() {
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    auto& v = global_workspaces();
+    if ((int)v.size() <= dev) v.resize(dev + 1, nullptr);
+    if (!v[dev]) v[dev] = new Workspace(dev);
+    return *v[dev];
+}
+
+void upload_pos4(Workspace& ws, int n, const float* pos, const float* mass = nullptr) {
+    std::vector<float4> h((size_t)n);
+    for (int i = 0; i < n; ++i)
+        h[i] = make_float4(pos[3 * i], pos[3 * i + 1], pos[3 * i + 2], mass ? mass[i] : 0.f);
+    ws.tmp4.ensure(n);
+    CK(cudaMemcpyAsync(ws.tmp4.p, h.data(), sizeof(float4) * n, cudaMemcpyHostToDevice, ws.stream));
+}
+
+}  // namespace
+
+// ============================================================== solver
+
+struct apbf_gpu_solver {
+    apbf_solver_config cfg;
+    Scene scene;
+    Workspace ws;
+    int n = 0;
+    SetBufs set[2];
+    SetBufs backup;
+    int cur = 0;
+    DBuf<float4> PB;
+    DBuf<int> order, nbrCount, nbr, tileCount, levelCount, activeCount, bucketStart;
+    DBuf<long long> groupBase;
+    DBuf<float4> sortedPM;
+    DBuf<float> stage;  // compact host<->device staging (13 words per particle)
+    DBuf<double> resid;
+    long long nbrCap = 0;
+    int numTiles = 0;
+    bool levels_valid = true;
+    bool metrics = true;
+    bool phase_timing = false;
+    float phase_ms[5] = {0, 0, 0, 0, 0};
+    cudaEvent_t ev[8];
+    apbf_iteration_observer observer = nullptr;
+    void* observer_user = nullptr;
+    // observer view of the in-flight state
+    bool in_iteration = false;
+    const float4* obs_xs = nullptr;
+    // derived config (solver.hpp:44-51), float as in SolverConfig<float>
+    float dt = 0, radius = 0, cap = 0;
+    int S = 0;
+    unsigned long long last_list_entries = 0, last_list_alloc = 0;
+    // per-launch CUDA-event timing of the lambda and delta-p kernels
+    bool kernel_timing = false;
+    std::vector<std::array<cudaEvent_t, 3>> kt_ev;
+    size_t kt_used = 0;
+    double kt_lambda_ms = 0, kt_deltap_ms = 0;
+    long long kt_launches = 0, kt_items = 0;
+
+    void enable_kernel_timing(bool on) {
+        kernel_timing = on;
+        const size_t need = (size_t)cfg.substeps * cfg.n_max;
+        while (on && kt_ev.size() < need) {
+            std::array<cudaEvent_t, 3> e;
+            for (auto& x : e) CK(cudaEventCreate(&x));
+            kt_ev.push_back(e);
+        }
+    }
+    void collect_kernel_timing(unsigned long long items) {
+        for (size_t k = 0; k < kt_used; ++k) {
+            float a = 0, b = 0;
+            CK(cudaEventElapsedTime(&a, kt_ev[k][0], kt_ev[k][1]));
+            CK(cudaEventElapsedTime(&b, kt_ev[k][1], kt_ev[k][2]));
+            kt_lambda_ms += a;
+            kt_deltap_ms += b;
+        }
+        kt_launches += (long long)kt_used;
+        kt_items += (long long)items;
+        kt_used = 0;
+    }
+
+    apbf_gpu_solver(const apbf_solver_config& c, const Scene& sc, int dev) : cfg(c), scene(sc), ws(dev) {
+        dt = cfg.dt_frame / (float)cfg.substeps;
+        radius = cfg.particle_radius > 0.0f ? cfg.particle_radius : cfg.h / 4.0f;
+        cap = cfg.velocity_cap > 0.0f ? cfg.velocity_cap : cfg.h / dt;
+        S = cfg.stab_threshold > 0 ? cfg.stab_threshold : cfg.n_max;
+        for (auto& e : ev) CK(cudaEventCreate(&e));
+        CK(cudaMemcpy(ws.scene.p, &scene, sizeof(Scene), cudaMemcpyHostToDevice));
+        levelCount.ensure(cfg.n_max + 2);
+        activeCount.ensure(cfg.n_max + 2);
+        bucketStart.ensure(cfg.n_max + 2);
+        resid.ensure((size_t)cfg.substeps * cfg.n_max);
+    }
+    ~apbf_gpu_solver() {
+        for (auto& e : ev) cudaEventDestroy(e);
+    }
+
+    void allocate(int nn) {
+        n = nn;
+        const size_t m = (size_t)std::max(nn, 1);
+        set[0].ensure(m);
+        set[1].ensure(m);
+        backup.ensure(m);
+        PB.ensure(m);
+        order.ensure(m);
+        const size_t groups = (m + 31) / 32 + 1;
+        nbrCount.ensure(groups * 32);
+        groupBase.ensure(groups);
+        if (nbrCap < (long long)m * 48 + 4096) {
+            nbrCap = (long long)m * 48 + 4096;
+            nbr.release();
+            nbr.ensure((size_t)nbrCap);
+        }
+        numTiles = (int)((m + kTileSize - 1) / kTileSize);
+        tileCount.ensure((size_t)(cfg.n_max + 1) * numTiles);
+        sortedPM.ensure(m);
+        stage.ensure(13 * m);
+        ws.ensure_particles(m);
+        ws.ensure_cells();
+    }
+
+    void copy_set(SetBufs& dst, SetBufs& src) {
+        const size_t m = (size_t)n;
+        cudaStream_t st = ws.stream;
+        CK(cudaMemcpyAsync(dst.X.p, src.X.p, sizeof(float4) * m, cudaMemcpyDeviceToDevice, st));
+        CK(cudaMemcpyAsync(dst.V.p, src.V.p, sizeof(float4) * m, cudaMemcpyDeviceToDevice, st));
+        CK(cudaMemcpyAsync(dst.XS.p, src.XS.p, sizeof(float4) * m, cudaMemcpyDeviceToDevice, st));
+        CK(cudaMemcpyAsync(dst.W.p, src.W.p, sizeof(float) * m, cudaMemcpyDeviceToDevice, st));
+        CK(cudaMemcpyAsync(dst.L.p, src.L.p, sizeof(float) * m, cudaMemcpyDeviceToDevice, st));
+        CK(cudaMemcpyAsync(dst.LV.p, src.LV.p, sizeof(int) * m, cudaMemcpyDeviceToDevice, st));
+    }
+
+    SolverConsts consts() const {
+        SolverConsts sc;
+        sc.kc = make_kernel_consts(cfg.h);
+        sc.invRho0 = 1.0f / cfg.rest_density;
+        sc.rho0 = cfg.rest_density;
+        sc.eps = cfg.epsilon;
+        sc.radius = radius;
+        sc.invRho0sq = sc.invRho0 * sc.invRho0;
+        return sc;
+    }
+
+    void mark(int k) {
+        if (phase_timing) CK(cudaEventRecord(ev[k], ws.stream));
+    }
+
+    // One frame on the device; returns after the control block is on the host.
+    void run_frame(bool assign_lod, const apbf_camera* cam, const apbf_lod_config* lod) {
+        cudaStream_t st = ws.stream;
+        Ctl* ctl = ws.ctl.p;
+        const SolverConsts sc = consts();
+        const int nMax = cfg.n_max;
+        CK(cudaEventRecord(ev[0], st));
+        kt_used = 0;
+        KL(k_frame_begin<<<1, 1, 0, st>>>(ctl));
+        if (assign_lod) {
+            if (cfg.mode == APBF_MODE_PBF) {
+                KL(k_fill_int<<<blocks(n, 256), 256, 0, st>>>(set[cur].LV.p, n, nMax));
+            } else {
+                apbf_lod_config lc = *lod;
+                lc.n_min = cfg.n_min;
+                lc.n_max = cfg.n_max;
+                run_lod(ws, set[cur].X.p, n, *cam, lc, radius, set[cur].LV.p);
+            }
+        }
+        mark(1);
+        for (int s = 0; s < cfg.substeps; ++s) {
+            StateSet src = set[cur].view(), dst = set[cur ^ 1].view();
+            KL(k_grid_reset<<<1, 1, 0, st>>>(ctl, 0));
+            KL(k_list_reset<<<1, 1, 0, st>>>(ctl));
+            KL(k_predict<<<blocks(n, 256), 256, 0, st>>>(n, src.X, src.V, src.XS, dt, cfg.gravity[0],
+                                                      cfg.gravity[1], cfg.gravity[2], ctl, s));
+            ws.run_grid(0, src.XS, n, cfg.h, cfg.h, scene.n > 0, radius);
+            const int smemG = (nMax + 1) * (int)sizeof(int);
+            KL(k_gather<<<numTiles, kTileThreads, smemG, st>>>(n, ctl, ws.perm.p, src, dst, nMax, numTiles,
+                                                           tileCount.p));
+            KL(k_level_scan<<<nMax + 1, 1024, 0, st>>>(ctl, numTiles, tileCount.p, levelCount.p));
+            KL(k_level_finish<<<1, 32, 0, st>>>(ctl, n, nMax, levelCount.p, activeCount.p, bucketStart.p));
+            KL(k_level_scatter<<<numTiles, kTileThreads, 9 * smemG, st>>>(n, ctl, dst.LV, nMax, numTiles,
+                                                                     tileCount.p, bucketStart.p, order.p));
+            KL(k_build_lists<<<blocks(n, 256), 256, 0, st>>>(n, ctl, order.p, dst.XS, ws.cellCount.p, cfg.h,
+                                                          cfg.h * cfg.h, nbr.p, nbrCount.p, groupBase.p,
+                                                          nbrCap));
+            if (S > 1)
+                KL(k_prestabilize<<<blocks(n, 256), 256, 0, st>>>(n, ctl, activeCount.p, S, order.p, dst.XS,
+                                                               dst.X, ws.scene.p, radius,
+                                                               cfg.stab_iterations, s));
+            LAUNCH_CHECK();
+            mark(2);
+            float4* P[2] = {dst.XS, PB.p};
+            int lastIter = nMax;
+            std::vector<int> hActive;
+            if (observer) {
+                hActive.resize(nMax + 2);
+                CK(cudaMemcpyAsync(hActive.data(), activeCount.p, sizeof(int) * (nMax + 2),
+                                   cudaMemcpyDeviceToHost, st));
+                CK(cudaStreamSynchronize(st));
+            }
+            for (int it = 1; it <= nMax; ++it) {
+                if (observer) {
+                    ws.read_ctl();
+                    if (ws.h_ctl->abort) break;
+                    if (hActive[it] == 0) {
+                        lastIter = it - 1;
+                        break;
+                    }
+                }
+                const float4* Pc = P[(it - 1) & 1];
+                float4* Pn = P[it & 1];
+                const int tslot = kernel_timing ? (int)kt_used++ : -1;
+                if (tslot >= 0) CK(cudaEventRecord(kt_ev[tslot][0], st));
+                KL(k_lambda<<<blocks(n, 256), 256, 0, st>>>(it, ctl, activeCount.p, order.p, Pc, dst.W,
+                                                         dst.L, nbr.p, nbrCount.p, groupBase.p, sc, s));
+                if (tslot >= 0) CK(cudaEventRecord(kt_ev[tslot][1], st));
+                if (cfg.inactive_lambda_zero)
+                    KL(k_deltap_apply<true><<<blocks(n, 256), 256, 0, st>>>(
+                        it, ctl, activeCount.p, order.p, Pc, Pn, dst.W, dst.L, dst.LV, nbr.p, nbrCount.p,
+                        groupBase.p, ws.scene.p, sc, s));
+                else
+                    KL(k_deltap_apply<false><<<blocks(n, 256), 256, 0, st>>>(
+                        it, ctl, activeCount.p, order.p, Pc, Pn, dst.W, dst.L, dst.LV, nbr.p, nbrCount.p,
+                        groupBase.p, ws.scene.p, sc, s));
+                if (tslot >= 0) CK(cudaEventRecord(kt_ev[tslot][2], st));
+                if (cfg.record_residuals) {
+                    CK(cudaMemsetAsync(resid.p + (size_t)s * nMax + (it - 1), 0, sizeof(double), st));
+                    KL(k_residual<<<blocks(n, 256), 256, 0, st>>>(n, it, ctl, activeCount.p, order.p, Pn,
+                                                               nbr.p, nbrCount.p, groupBase.p, sc,
+                                                               resid.p + (size_t)s * nMax + (it - 1)));
+                }
+                LAUNCH_CHECK();
+                if (observer) {
+                    ws.read_ctl();
+                    if (ws.h_ctl->abort) break;
+                    in_iteration = true;
+                    obs_xs = Pn;
+                    const int c = cur;
+                    cur ^= 1;  // expose dst as the current set to get_state
+                    observer(observer_user, s, it);
+                    cur = c;
+                    in_iteration = false;
+                }
+            }
+            mark(3);
+            float4* Pf = P[lastIter & 1];
+            KL(k_finalize<<<blocks(n, 256), 256, 0, st>>>(n, ctl, Pf, dst.XS, dst.X, dst.V, dt, cap,
+                                                       Pf != dst.XS ? 1 : 0, s));
+            LAUNCH_CHECK();
+            cur ^= 1;
+            mark(4);
+        }
+        CK(cudaEventRecord(ev[5], st));
+        if (metrics) {
+            // allDensities(x) over a throwaway grid (solver.hpp:271-279).
+            KL(k_grid_reset<<<1, 1, 0, st>>>(ctl, 1));
+            KL(k_aabb<<<blocks(n, 256), 256, 0, st>>>(n, set[cur].X.p, ctl, 1));
+            ws.run_grid(1, set[cur].X.p, n, cfg.h, cfg.h, false, radius);
+            KL(k_gather_posmass<<<blocks(n, 256), 256, 0, st>>>(n, ctl, ws.perm.p, set[cur].X.p,
+                                                             set[cur].XS.p, sortedPM.p));
+            KL(k_density_stats<<<blocks(n, 256), 256, 0, st>>>(n, ctl, sortedPM.p, ws.cellCount.p, sc.kc));
+            LAUNCH_CHECK();
+        }
+        CK(cudaEventRecord(ev[6], st));
+        ws.read_ctl();
+    }
+
+    void frame(bool assign_lod, const apbf_camera* cam, const apbf_lod_config* lod, int frame_index,
+               apbf_frame_stats* out) {
+        CK(cudaSetDevice(ws.device));
+        if (assign_lod && cfg.mode == APBF_MODE_APBF) {
+            apbf_lod_config lc = *lod;
+            validate_lod(lc);
+            if (n > 0 && lc.model == APBF_LOD_DTVS) {
+                if (!(radius > 0.0f)) fail(APBF_ERR_INVALID_ARGUMENT, "splat radius must be positive");
+                (void)make_frame(*cam);  // camera validation (depth_splat.hpp:29-42, 59-63)
+            }
+        }
+        apbf_frame_stats st;
+        std::memset(&st, 0, sizeof st);
+        st.frame = frame_index;
+        if (n == 0) {
+            if (out) {
+                double* r = out->residuals;
+                int rc = out->residuals_capacity;
+                *out = st;
+                out->residuals = r;
+                out->residuals_capacity = rc;
+            }
+            return;
+        }
+        const int start_set = cur;
+        copy_set(backup, set[start_set]);
+        for (int attempt = 0;; ++attempt) {
+            run_frame(assign_lod, cam, lod);
+            if (!ws.h_ctl->list_overflow) break;
+            // Neighbour storage too small: restore the frame-start state,
+            // double the capacity and run the frame again.
+            if (attempt > 6) fail(APBF_ERR_RUNTIME, "neighbor list overflow");
+            cur = start_set;
+            copy_set(set[cur], backup);
+            nbrCap *= 2;
+            nbr.release();
+            nbr.ensure((size_t)nbrCap);
+        }
+        const Ctl& c = *ws.h_ctl;
+        if (kernel_timing) collect_kernel_timing(c.total_iterations);
+        last_list_entries = c.list_entries;
+        last_list_alloc = c.list_alloc;
+        if (c.runtime_error) fail(APBF_ERR_RUNTIME, "grid cell count exceeds limit; domain blew up");
+        static const char* names[kNumPassSlots] = {"predict", "prestabilize", "lambda",
+                                                   "apply",   "finalize",     "finalize"};
+        static const char* details[kNumPassSlots] = {
+            "non-finite predicted position", "non-finite predicted position", "non-finite lambda",
+            "non-finite predicted position", "non-finite velocity",           "non-finite position"};
+        // The earliest failing pass: they abort the frame, so only one pass
+        // (finalize: velocity before position) can hold a record.
+        for (int s = 0; s < kNumPassSlots; ++s)
+            if (c.bad[s] != 0x7fffffff) numerical(names[s], c.bad[s], details[s]);
+        float ms = 0.f;
+        CK(cudaEventElapsedTime(&ms, ev[0], ev[5]));
+        st.wall_ms = ms;
+        st.total_iterations = (int64_t)c.total_iterations;
+        st.contacts = (int64_t)c.contacts;
+        if (metrics) {
+            const double scale = 100.0 / (double)cfg.rest_density;
+            st.avg_density_pct = c.rho_sum / n * scale;
+            st.min_density_pct = (double)ord2f(c.rho_min_ord) * scale;
+            st.max_density_pct = (double)ord2f(c.rho_max_ord) * scale;
+        }
+        if (cfg.record_residuals) {
+            std::vector<double> r((size_t)cfg.substeps * cfg.n_max);
+            CK(cudaMemcpy(r.data(), resid.p, sizeof(double) * r.size(), cudaMemcpyDeviceToHost));
+            // executed iterations per substep = max level present; the
+            // totalIterations sum cannot tell us, so recompute from levels
+            // (levels are frame-constant).
+            std::vector<int> lv((size_t)n);
+            CK(cudaMemcpy(lv.data(), set[cur].LV.p, sizeof(int) * n, cudaMemcpyDeviceToHost));
+            int maxl = 0;
+            for (int v : lv) maxl = std::max(maxl, v);
+            int k = 0;
+            for (int s = 0; s < cfg.substeps; ++s)
+                for (int it = 1; it <= maxl; ++it, ++k) {
+                    if (out && out->residuals && k < out->residuals_capacity)
+                        out->residuals[k] = r[(size_t)s * cfg.n_max + (it - 1)] / n;
+                }
+            st.n_residuals = k;
+        }
+        if (phase_timing) {
+            float t[5] = {0, 0, 0, 0, 0};
+            cudaEventElapsedTime(&t[0], ev[0], ev[1]);
+            cudaEventElapsedTime(&t[4], ev[5], ev[6]);
+            phase_ms[0] = t[0];
+            phase_ms[4] = t[4];
+            // per-phase split of the last substep scaled to all substeps
+            float a = 0, b = 0, d = 0;
+            cudaEventElapsedTime(&a, ev[1], ev[2]);
+            cudaEventElapsedTime(&b, ev[2], ev[3]);
+            cudaEventElapsedTime(&d, ev[3], ev[4]);
+            phase_ms[1] = a;
+            phase_ms[2] = b;
+            phase_ms[3] = d;
+        }
+        if (out) {
+            double* r = out->residuals;
+            int rc = out->residuals_capacity;
+            *out = st;
+            out->residuals = r;
+            out->residuals_capacity = rc;
+        }
+    }
+};
+
+// =============================================================== C-ABI
+
+extern "C" {
+
+int32_t apbf_gpu_abi_version(void) { return APBF_GPU_ABI_VERSION; }
+
+int32_t apbf_gpu_device_count(void) {
+    int c = 0;
+    if (cudaGetDeviceCount(&c) != cudaSuccess) return 0;
+    return c;
+}
+
+static void validate_config(const apbf_solver_config* c) {
+    if (c->n_min < 1 || c->n_max < c->n_min)
+        fail(APBF_ERR_INVALID_ARGUMENT, "iteration range requires 1 <= n_min <= n_max");
+    if (!(c->dt_frame > 0.0f)) fail(APBF_ERR_INVALID_ARGUMENT, "dt_frame must be positive");
+    if (c->substeps < 1) fail(APBF_ERR_INVALID_ARGUMENT, "substeps must be at least 1");
+    if (!(c->rest_density > 0.0f)) fail(APBF_ERR_INVALID_ARGUMENT, "rest density must be positive");
+    if (!(c->h > 0.0f)) fail(APBF_ERR_INVALID_ARGUMENT, "smoothing length must be positive");
+    if (c->epsilon < 0.0f) fail(APBF_ERR_INVALID_ARGUMENT, "epsilon must be non-negative");
+    if (c->stab_iterations < 0) fail(APBF_ERR_INVALID_ARGUMENT, "stab iterations must be non-negative");
+    if (c->stab_threshold != 0 && (c->stab_threshold < 1 || c->stab_threshold > c->n_max))
+        fail(APBF_ERR_INVALID_ARGUMENT, "stab threshold must lie in [1, n_max]");
+    if (c->particle_radius < 0.0f) fail(APBF_ERR_INVALID_ARGUMENT, "particle radius must be non-negative");
+    if (c->velocity_cap < 0.0f) fail(APBF_ERR_INVALID_ARGUMENT, "velocity cap must be non-negative");
+    if (!finite3h(c->gravity)) fail(APBF_ERR_INVALID_ARGUMENT, "gravity must be finite");
+    if (c->mode != APBF_MODE_PBF && c->mode != APBF_MODE_APBF)
+        fail(APBF_ERR_INVALID_ARGUMENT, "unknown solver mode");
+    if (c->n_max > 4096) fail(APBF_ERR_INVALID_ARGUMENT, "n_max above the GPU level-table limit (4096)");
+}
+
+int32_t apbf_gpu_solver_create(const apbf_solver_config* cfg, const apbf_sdf_primitive* prims,
+                               int32_t n_prims, float gradient_step, int32_t device,
+                               apbf_gpu_solver** out, apbf_error* err) {
+    return guarded(err, [&] {
+        *out = nullptr;
+        validate_config(cfg);
+        const Scene sc = make_scene(prims, n_prims, gradient_step);
+        int count = 0;
+        CK(cudaGetDeviceCount(&count));
+        if (device < 0 || device >= count) fail(APBF_ERR_INVALID_ARGUMENT, "CUDA device out of range");
+        CK(cudaSetDevice(device));
+        *out = new apbf_gpu_solver(*cfg, sc, device);
+    });
+}
+
+void apbf_gpu_solver_destroy(apbf_gpu_solver* s) {
+    if (!s) return;
+    cudaSetDevice(s->ws.device);
+    cudaStreamSynchronize(s->ws.stream);
+    delete s;
+}
+
+int32_t apbf_gpu_set_state(apbf_gpu_solver* s, int32_t n, const float* x, const float* xs,
+                           const float* v, const float* mass, const float* inv_mass,
+                           const float* lambda, const int32_t* level, apbf_error* err) {
+    return guarded(err, [&] {
+        if (n < 0) fail(APBF_ERR_INVALID_ARGUMENT, "negative particle count");
+        CK(cudaSetDevice(s->ws.device));
+        s->allocate(n);
+        s->cur = 0;
+        s->levels_valid = true;
+        if (n == 0) return;
+        bool lv_ok = true;
+        for (int i = 0; i < n; ++i) lv_ok = lv_ok && level[i] >= s->cfg.n_min && level[i] <= s->cfg.n_max;
+        s->levels_valid = lv_ok;
+        // Caller arrays go straight to the device staging area (DMA from the
+        // caller's memory: full PCIe rate when it is pinned), then one kernel
+        // unpacks them into the float4 SoA layout.
+        cudaStream_t st = s->ws.stream;
+        float* d = s->stage.p;
+        const size_t n1 = sizeof(float) * (size_t)n, n3 = 3 * n1;
+        CK(cudaMemcpyAsync(d, x, n3, cudaMemcpyHostToDevice, st));
+        CK(cudaMemcpyAsync(d + 3LL * n, xs, n3, cudaMemcpyHostToDevice, st));
+        CK(cudaMemcpyAsync(d + 6LL * n, v, n3, cudaMemcpyHostToDevice, st));
+        CK(cudaMemcpyAsync(d + 9LL * n, mass, n1, cudaMemcpyHostToDevice, st));
+        CK(cudaMemcpyAsync(d + 10LL * n, inv_mass, n1, cudaMemcpyHostToDevice, st));
+        CK(cudaMemcpyAsync(d + 11LL * n, lambda, n1, cudaMemcpyHostToDevice, st));
+        CK(cudaMemcpyAsync(d + 12LL * n, level, n1, cudaMemcpyHostToDevice, st));
+        KL(k_unpack_state<<<blocks(n, 256), 256, 0, st>>>(n, d, s->set[0].view()));
+        LAUNCH_CHECK();
+        CK(cudaStreamSynchronize(st));
+    });
+}
+
+int32_t apbf_gpu_get_state(apbf_gpu_solver* s, float* x, float* xs, float* v, float* mass,
+                           float* inv_mass, float* lambda, int32_t* level, apbf_error* err) {
+    return guarded(err, [&] {
+        CK(cudaSetDevice(s->ws.device));
+        const int n = s->n;
+        if (n == 0) return;
+        cudaStream_t st = s->ws.stream;
+        SetBufs& b = s->set[s->cur];
+        const float4* dxs = (s->in_iteration && s->obs_xs) ? s->obs_xs : b.XS.p;
+        float* d = s->stage.p;
+        KL(k_pack_state<<<blocks(n, 256), 256, 0, st>>>(n, b.view(), dxs, d));
+        LAUNCH_CHECK();
+        const size_t n1 = sizeof(float) * (size_t)n, n3 = 3 * n1;
+        if (x) CK(cudaMemcpyAsync(x, d, n3, cudaMemcpyDeviceToHost, st));
+        if (xs) CK(cudaMemcpyAsync(xs, d + 3LL * n, n3, cudaMemcpyDeviceToHost, st));
+        if (v) CK(cudaMemcpyAsync(v, d + 6LL * n, n3, cudaMemcpyDeviceToHost, st));
+        if (mass) CK(cudaMemcpyAsync(mass, d + 9LL * n, n1, cudaMemcpyDeviceToHost, st));
+        if (inv_mass) CK(cudaMemcpyAsync(inv_mass, d + 10LL * n, n1, cudaMemcpyDeviceToHost, st));
+        if (lambda) CK(cudaMemcpyAsync(lambda, d + 11LL * n, n1, cudaMemcpyDeviceToHost, st));
+        if (level) CK(cudaMemcpyAsync(level, d + 12LL * n, n1, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+    });
+}
+
+void* apbf_gpu_stream(const apbf_gpu_solver* s) { return (void*)s->ws.stream; }
+
+int32_t apbf_gpu_particle_count(const apbf_gpu_solver* s) { return s ? s->n : 0; }
+
+int32_t apbf_gpu_step_frame(apbf_gpu_solver* s, const apbf_camera* cam, const apbf_lod_config* lod,
+                            int32_t frame_index, apbf_frame_stats* out, apbf_error* err) {
+    return guarded(err, [&] {
+        s->frame(true, cam, lod, frame_index, out);
+        s->levels_valid = true;
+    });
+}
+
+int32_t apbf_gpu_step_frame_with_levels(apbf_gpu_solver* s, int32_t frame_index, apbf_frame_stats* out,
+                                        apbf_error* err) {
+    return guarded(err, [&] {
+        if (!s->levels_valid)
+            fail(APBF_ERR_INVALID_ARGUMENT, "particle level outside configured iteration range");
+        s->frame(false, nullptr, nullptr, frame_index, out);
+    });
+}
+
+int32_t apbf_gpu_set_iteration_observer(apbf_gpu_solver* s, apbf_iteration_observer cb, void* user) {
+    s->observer = cb;
+    s->observer_user = user;
+    return APBF_OK;
+}
+
+int32_t apbf_gpu_set_frame_metrics(apbf_gpu_solver* s, int32_t enabled) {
+    s->metrics = enabled != 0;
+    return APBF_OK;
+}
+
+int32_t apbf_gpu_set_phase_timing(apbf_gpu_solver* s, int32_t enabled) {
+    s->phase_timing = enabled != 0;
+    return APBF_OK;
+}
+
+int32_t apbf_gpu_last_phase_ms(const apbf_gpu_solver* s, float* out5) {
+    for (int k = 0; k < 5; ++k) out5[k] = s->phase_ms[k];
+    return APBF_OK;
+}
+
+int32_t apbf_gpu_set_kernel_timing(apbf_gpu_solver* s, int32_t enabled, apbf_error* err) {
+    return guarded(err, [&] {
+        CK(cudaSetDevice(s->ws.device));
+        s->enable_kernel_timing(enabled != 0);
+        s->kt_lambda_ms = s->kt_deltap_ms = 0;
+        s->kt_launches = s->kt_items = 0;
+    });
+}
+
+int32_t apbf_gpu_kernel_times(const apbf_gpu_solver* s, double* lambda_ms, double* deltap_ms,
+                              int64_t* launches, int64_t* particle_iterations) {
+    if (lambda_ms) *lambda_ms = s->kt_lambda_ms;
+    if (deltap_ms) *deltap_ms = s->kt_deltap_ms;
+    if (launches) *launches = s->kt_launches;
+    if (particle_iterations) *particle_iterations = s->kt_items;
+    return APBF_OK;
+}
+
+uint64_t apbf_gpu_launch_count(void) { return g_launches; }
+
+int32_t apbf_gpu_last_neighbor_stats(const apbf_gpu_solver* s, int64_t* total_entries,
+                                     int64_t* list_capacity) {
+    if (total_entries) *total_entries = (int64_t)s->last_list_entries;
+    if (list_capacity) *list_capacity = (int64_t)s->last_list_alloc;
+    return APBF_OK;
+}
+
+// ----------------------------------------------------- component calls
+
+static void check_grid_args(int n, const float* pos, float h, float pad) {
+    if (!(h > 0.0f)) fail(APBF_ERR_INVALID_ARGUMENT, "grid cell size must be positive");
+    if (pad < 0.0f) fail(APBF_ERR_INVALID_ARGUMENT, "grid padding must be non-negative");
+    for (int i = 0; i < n; ++i)
+        if (!finite3h(pos + 3 * i)) numerical("grid build", i, "non-finite position");
+}
+
+// Builds grid g on the uploaded tmp4 positions; returns host Ctl.
+static void component_grid(Workspace& ws, int g, int n, float h, float pad) {
+    cudaStream_t st = ws.stream;
+    KL(k_frame_begin<<<1, 1, 0, st>>>(ws.ctl.p));
+    KL(k_grid_reset<<<1, 1, 0, st>>>(ws.ctl.p, g));
+    KL(k_aabb<<<blocks(n, 256), 256, 0, st>>>(n, ws.tmp4.p, ws.ctl.p, g));
+    ws.run_grid(g, ws.tmp4.p, n, h, pad, false, 0.f);
+    ws.read_ctl();
+    if (ws.h_ctl->runtime_error) fail(APBF_ERR_RUNTIME, "grid cell count exceeds limit; domain blew up");
+}
+
+int32_t apbf_gpu_grid_build(int32_t n, const float* positions, float h, float padding, int32_t* perm,
+                            float* origin, int32_t* dims, int32_t* cell_start,
+                            int64_t cell_start_capacity, int64_t* cells_out, apbf_error* err) {
+    return guarded(err, [&] {
+        check_grid_args(n, positions, h, padding);
+        if (n == 0) {
+            if (origin) origin[0] = origin[1] = origin[2] = 0.f;
+            if (dims) dims[0] = dims[1] = dims[2] = 1;
+            if (cells_out) *cells_out = 1;
+            if (cell_start && cell_start_capacity >= 2) cell_start[0] = cell_start[1] = 0;
+            return;
+        }
+        Workspace& ws = component_ws();
+        upload_pos4(ws, n, positions);
+        component_grid(ws, 0, n, h, padding);
+        const GridDev& G = ws.h_ctl->grid[0];
+        if (origin)
+            for (int a = 0; a < 3; ++a) origin[a] = G.origin[a];
+        if (dims)
+            for (int a = 0; a < 3; ++a) dims[a] = G.dims[a];
+        if (cells_out) *cells_out = G.cells;
+        if (perm) CK(cudaMemcpy(perm, ws.perm.p, sizeof(int) * n, cudaMemcpyDeviceToHost));
+        if (cell_start) {
+            if (cell_start_capacity < G.cells + 1)
+                fail(APBF_ERR_INVALID_ARGUMENT, "cell_start capacity too small");
+            CK(cudaMemcpy(cell_start, ws.cellCount.p, sizeof(int) * (G.cells + 1), cudaMemcpyDeviceToHost));
+        }
+    });
+}
+
+int32_t apbf_gpu_neighbor_lists(int32_t n, const float* positions, float h, float padding,
+                                int32_t* offsets, int32_t* indices, int64_t indices_capacity,
+                                int64_t* total_out, apbf_error* err) {
+    return guarded(err, [&] {
+        check_grid_args(n, positions, h, padding);
+        if (n == 0) {
+            if (offsets) offsets[0] = 0;
+            if (total_out) *total_out = 0;
+            return;
+        }
+        Workspace& ws = component_ws();
+        upload_pos4(ws, n, positions);
+        component_grid(ws, 0, n, h, padding);
+        // sorted points (the grid's points_ copy) and identity order
+        DBuf<float4> sorted;
+        sorted.ensure(n);
+        DBuf<int> order, cnt, nb;
+        DBuf<long long> gb;
+        order.ensure(n);
+        const size_t groups = ((size_t)n + 31) / 32 + 1;
+        cnt.ensure(groups * 32);
+        gb.ensure(groups);
+        long long cap = (long long)n * 64 + 4096;
+        cudaStream_t st = ws.stream;
+        KL(k_gather_posmass<<<blocks(n, 256), 256, 0, st>>>(n, ws.ctl.p, ws.perm.p, ws.tmp4.p, ws.tmp4.p,
+                                                         sorted.p));
+        std::vector<int> iota(n);
+        for (int i = 0; i < n; ++i) iota[i] = i;
+        CK(cudaMemcpyAsync(order.p, iota.data(), sizeof(int) * n, cudaMemcpyHostToDevice, st));
+        for (;;) {
+            nb.release();
+            nb.ensure((size_t)cap);
+            KL(k_list_reset<<<1, 1, 0, st>>>(ws.ctl.p));
+            KL(k_build_lists<<<blocks(n, 256), 256, 0, st>>>(n, ws.ctl.p, order.p, sorted.p, ws.cellCount.p,
+                                                          h, h * h, nb.p, cnt.p, gb.p, cap));
+            LAUNCH_CHECK();
+            ws.read_ctl();
+            if (!ws.h_ctl->list_overflow) break;
+            KL(k_frame_begin<<<1, 1, 0, st>>>(ws.ctl.p));  // clear the abort of the overflowed build
+            cap *= 2;
+        }
+        std::vector<int> hc(n);
+        std::vector<long long> hg(groups);
+        const long long alloc = (long long)ws.h_ctl->list_alloc;
+        std::vector<int> hn((size_t)std::max<long long>(alloc, 1));
+        CK(cudaMemcpy(hc.data(), cnt.p, sizeof(int) * n, cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(hg.data(), gb.p, sizeof(long long) * groups, cudaMemcpyDeviceToHost));
+        if (alloc > 0) CK(cudaMemcpy(hn.data(), nb.p, sizeof(int) * alloc, cudaMemcpyDeviceToHost));
+        long long total = 0;
+        for (int i = 0; i < n; ++i) total += hc[i];
+        if (total_out) *total_out = total;
+        if (offsets) {
+            offsets[0] = 0;
+            for (int i = 0; i < n; ++i) offsets[i + 1] = offsets[i] + hc[i];
+        }
+        if (indices) {
+            if (indices_capacity < total) fail(APBF_ERR_INVALID_ARGUMENT, "indices capacity too small");
+            long long w = 0;
+            for (int i = 0; i < n; ++i)
+                for (int e = 0; e < hc[i]; ++e) indices[w++] = hn[hg[i >> 5] + (long long)e * 32 + (i & 31)];
+        }
+    });
+}
+
+int32_t apbf_gpu_all_densities(int32_t n, const float* positions, const float* masses, float h,
+                               float* rho_out, apbf_error* err) {
+    return guarded(err, [&] {
+        if (n == 0) return;
+        check_grid_args(n, positions, h, h);
+        Workspace& ws = component_ws();
+        upload_pos4(ws, n, positions, masses);
+        component_grid(ws, 1, n, h, h);
+        DBuf<float4> sorted;
+        DBuf<float> rho;
+        sorted.ensure(n);
+        rho.ensure(n);
+        cudaStream_t st = ws.stream;
+        KL(k_gather_posmass<<<blocks(n, 256), 256, 0, st>>>(n, ws.ctl.p, ws.perm.p, ws.tmp4.p, ws.tmp4.p,
+                                                         sorted.p));
+        KL(k_density_out<<<blocks(n, 256), 256, 0, st>>>(n, ws.ctl.p, sorted.p, ws.perm.p, ws.cellCount.p,
+                                                      make_kernel_consts(h), rho.p));
+        LAUNCH_CHECK();
+        CK(cudaMemcpyAsync(rho_out, rho.p, sizeof(float) * n, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+    });
+}
+
+static void component_lod(int n, const float* positions, const apbf_camera* cam,
+                          const apbf_lod_config* lod, float radius, int32_t* levels_out) {
+    validate_lod(*lod);
+    if (lod->n_min < 1 || lod->n_max < lod->n_min)
+        fail(APBF_ERR_INVALID_ARGUMENT, "iteration range requires 1 <= n_min <= n_max");
+    if (n == 0) return;
+    if (lod->model == APBF_LOD_DTVS) {
+        if (!(radius > 0.0f)) fail(APBF_ERR_INVALID_ARGUMENT, "splat radius must be positive");
+        (void)make_frame(*cam);
+    }
+    Workspace& ws = component_ws();
+    upload_pos4(ws, n, positions);
+    DBuf<int> lv;
+    lv.ensure(n);
+    KL(k_frame_begin<<<1, 1, 0, ws.stream>>>(ws.ctl.p));
+    run_lod(ws, ws.tmp4.p, n, *cam, *lod, radius, lv.p);
+    CK(cudaMemcpyAsync(levels_out, lv.p, sizeof(int) * n, cudaMemcpyDeviceToHost, ws.stream));
+    CK(cudaStreamSynchronize(ws.stream));
+}
+
+int32_t apbf_gpu_lod_dtc(int32_t n, const float* positions, const apbf_camera* cam,
+                         const apbf_lod_config* lod, int32_t* levels_out, apbf_error* err) {
+    return guarded(err, [&] {
+        apbf_lod_config l = *lod;
+        l.model = APBF_LOD_DTC;
+        component_lod(n, positions, cam, &l, 0.f, levels_out);
+    });
+}
+
+int32_t apbf_gpu_lod_dtvs(int32_t n, const float* positions, const apbf_camera* cam,
+                          const apbf_lod_config* lod, float radius, int32_t* levels_out,
+                          apbf_error* err) {
+    return guarded(err, [&] {
+        apbf_lod_config l = *lod;
+        l.model = APBF_LOD_DTVS;
+        component_lod(n, positions, cam, &l, radius, levels_out);
+    });
+}
+
+int32_t apbf_gpu_splat(int32_t n, const float* positions, float radius, const apbf_camera* cam,
+                       float* depth_out, apbf_error* err) {
+    return guarded(err, [&] {
+        if (!(radius > 0.0f)) fail(APBF_ERR_INVALID_ARGUMENT, "splat radius must be positive");
+        const CamFrame f = make_frame(*cam);
+        Workspace& ws = component_ws();
+        const size_t px = (size_t)cam->width * cam->height;
+        ws.depth.ensure(px);
+        KL(k_fill_int<<<blocks((long long)px, 256), 256, 0, ws.stream>>>(ws.depth.p, (int)px, 0x7f800000));
+        if (n > 0) {
+            upload_pos4(ws, n, positions);
+            KL(k_splat<<<blocks(n, 256), 256, 0, ws.stream>>>(n, ws.tmp4.p, radius, f, ws.depth.p));
+        }
+        LAUNCH_CHECK();
+        CK(cudaMemcpyAsync(depth_out, ws.depth.p, sizeof(float) * px, cudaMemcpyDeviceToHost, ws.stream));
+        CK(cudaStreamSynchronize(ws.stream));
+    });
+}
+
+int32_t apbf_gpu_count_contacts(int32_t n, const float* positions, const apbf_sdf_primitive* prims,
+                                int32_t n_prims, float gradient_step, float radius, int64_t* count_out,
+                                apbf_error* err) {
+    return guarded(err, [&] {
+        const Scene sc = make_scene(prims, n_prims, gradient_step);
+        *count_out = 0;
+        if (n == 0 || sc.n == 0) return;
+        Workspace& ws = component_ws();
+        CK(cudaMemcpyAsync(ws.scene.p, &sc, sizeof(Scene), cudaMemcpyHostToDevice, ws.stream));
+        upload_pos4(ws, n, positions);
+        KL(k_frame_begin<<<1, 1, 0, ws.stream>>>(ws.ctl.p));
+        KL(k_count_contacts<<<blocks(n, 256), 256, 0, ws.stream>>>(n, ws.tmp4.p, ws.scene.p, radius, ws.ctl.p));
+        LAUNCH_CHECK();
+        ws.read_ctl();
+        *count_out = (int64_t)ws.h_ctl->contacts;
+    });
+}
+
+}  // extern "C"

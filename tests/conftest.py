@@ -1,0 +1,12 @@
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+
+def pytest_configure(config):
+    config.addinivalue_line("markers", "gpu: needs a CUDA device (B200); parity tests proper")
+    config.addinivalue_line("markers", "ref: needs oracle/_ref (the reference compiled from /root/reference)")
+    config.addinivalue_line("markers", "slow: long-running")

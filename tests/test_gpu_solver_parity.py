@@ -1,0 +1,67 @@
+"""GPU solver vs the CPU oracle, bit for bit (SURVEY.md 8c tier A).
+
+Every frame compares the whole ParticleSet (storage order included: the
+solver leaves the state in the last substep's cell order, uniform_grid.hpp:
+102-105) and the integer frame stats.  Sizes are small enough for the oracle.
+"""
+import numpy as np
+import pytest
+
+from oracle.oracle import OracleSolver
+from paper_1608_04721_b200 import (IterationRange, LodModel, Solver, SolverMode)
+from paper_1608_04721_b200 import scenario as S
+
+pytestmark = pytest.mark.gpu
+
+FIELDS = ("x", "x_star", "v", "mass", "inv_mass", "lambda_", "level")
+
+
+def assert_same_state(a, b, where):
+    for k in FIELDS:
+        ga, gb = getattr(a, k), getattr(b, k)
+        assert ga.shape == gb.shape, (where, k)
+        if not np.array_equal(ga, gb):
+            bad = np.argwhere(ga != gb)
+            raise AssertionError(f"{where}: field {k} differs at {bad[:5].tolist()} "
+                                 f"({len(bad)} entries)")
+
+
+def run_pair(spec, frames, seed=1):
+    gpu = Solver(spec.solver, spec.scene)
+    orc = OracleSolver(spec.solver, spec.scene)
+    a = S.make_state(spec, seed)
+    b = a.copy()
+    for f in range(frames):
+        sa = gpu.step_frame(a, spec.camera, spec.lod, f)
+        sb = orc.step_frame(b, spec.camera, spec.lod, f)
+        assert_same_state(a, b, f"frame {f}")
+        assert sa.total_iterations == sb.total_iterations
+        assert sa.contacts == sb.contacts
+        assert sa.min_density_pct == sb.min_density_pct
+        assert sa.max_density_pct == sb.max_density_pct
+        assert sa.avg_density_pct == pytest.approx(sb.avg_density_pct, rel=1e-9)
+    return a, sa
+
+
+@pytest.mark.parametrize("mode,model", [(SolverMode.PBF, LodModel.DTC),
+                                        (SolverMode.APBF, LodModel.DTC),
+                                        (SolverMode.APBF, LodModel.DTVS)])
+def test_dam_break_c1_bitwise(mode, model):
+    """C1: dam break 25^3 = 15,625 particles, PBF N=5 and APBF {5..10}."""
+    spec = S.build_scenario("dam_break", 15625 / 216000)
+    spec.solver.mode = mode
+    spec.solver.range = IterationRange(5, 5) if mode == SolverMode.PBF else IterationRange(5, 10)
+    spec.lod.model = model
+    spec.lod.range = spec.solver.range
+    run_pair(spec, 10)
+
+
+def test_double_dam_break_bitwise():
+    spec = S.build_scenario("double_dam_break", 0.05)
+    run_pair(spec, 4)
+
+
+def test_multi_dam_break_cone_bitwise():
+    """Cone SDF (glibc hypotf reproduced on the device) + box."""
+    spec = S.build_scenario("multi_dam_break", 0.1)
+    run_pair(spec, 4)
