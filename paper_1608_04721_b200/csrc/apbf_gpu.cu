@@ -5,6 +5,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <stdexcept>
 #include <string>
@@ -340,6 +341,7 @@ struct apbf_gpu_solver {
     DBuf<float4> PB;
     DBuf<int> order, nbrCount, nbr, tileCount, levelCount, activeCount, bucketStart;
     DBuf<long long> groupBase;
+    DBuf<float> coef;  // per-list-entry spiky coefficient, lambda -> delta-p
     DBuf<float4> sortedPM;
     DBuf<float> stage;  // compact host<->device staging (13 words per particle)
     DBuf<double> resid;
@@ -394,6 +396,8 @@ struct apbf_gpu_solver {
         cap = cfg.velocity_cap > 0.0f ? cfg.velocity_cap : cfg.h / dt;
         S = cfg.stab_threshold > 0 ? cfg.stab_threshold : cfg.n_max;
         for (auto& e : ev) CK(cudaEventCreate(&e));
+        if (const char* v = std::getenv("APBF_STAGE_LISTS")) use_stage = std::atoi(v) != 0;
+        if (const char* v = std::getenv("APBF_COEF_CACHE")) use_coef = std::atoi(v) != 0;
         CK(cudaMemcpy(ws.scene.p, &scene, sizeof(Scene), cudaMemcpyHostToDevice));
         levelCount.ensure(cfg.n_max + 2);
         activeCount.ensure(cfg.n_max + 2);
@@ -419,6 +423,8 @@ struct apbf_gpu_solver {
             nbrCap = (long long)m * 48 + 4096;
             nbr.release();
             nbr.ensure((size_t)nbrCap);
+            coef.release();
+            coef.ensure((size_t)nbrCap);
         }
         numTiles = (int)((m + kTileSize - 1) / kTileSize);
         tileCount.ensure((size_t)(cfg.n_max + 1) * numTiles);
@@ -448,6 +454,43 @@ struct apbf_gpu_solver {
         sc.radius = radius;
         sc.invRho0sq = sc.invRho0 * sc.invRho0;
         return sc;
+    }
+
+    // Variant switches for A/B measurements: APBF_STAGE_LISTS=1 stages list
+    // slabs in shared memory (bulk async copy); APBF_COEF_CACHE=0 makes the
+    // delta-p pass recompute the spiky coefficients instead of reading the
+    // lambda pass's cache.  Every variant is bit-identical.
+    bool use_stage = false, use_coef = true;
+
+    template <bool kZ, bool kS, bool kC>
+    void launch_pair_t(int it, int s, const float4* Pc, float4* Pn, const StateSet& dst,
+                       const SolverConsts& sc, int tslot) {
+        cudaStream_t st = ws.stream;
+        Ctl* ctl = ws.ctl.p;
+        const int sb = blocks(n, kSolverThreads);
+        const int smem = kS ? kSolverSmem : 0;
+        KL(k_lambda<kS, kC><<<sb, kSolverThreads, smem, st>>>(n, it, ctl, activeCount.p, order.p, Pc,
+                                                               dst.W, dst.L, nbr.p, nbrCount.p,
+                                                               groupBase.p, coef.p, sc, s));
+        if (tslot >= 0) CK(cudaEventRecord(kt_ev[tslot][1], st));
+        KL(k_deltap_apply<kZ, kS, kC><<<sb, kSolverThreads, smem, st>>>(
+            n, it, ctl, activeCount.p, order.p, Pc, Pn, dst.W, dst.L, dst.LV, nbr.p, nbrCount.p,
+            groupBase.p, coef.p, ws.scene.p, sc, s));
+    }
+
+    void launch_solver_pair(int it, int s, const float4* Pc, float4* Pn, const StateSet& dst,
+                            const SolverConsts& sc, int tslot) {
+        const int v = (cfg.inactive_lambda_zero ? 4 : 0) | (use_stage ? 2 : 0) | (use_coef ? 1 : 0);
+        switch (v) {
+            case 0: launch_pair_t<false, false, false>(it, s, Pc, Pn, dst, sc, tslot); break;
+            case 1: launch_pair_t<false, false, true>(it, s, Pc, Pn, dst, sc, tslot); break;
+            case 2: launch_pair_t<false, true, false>(it, s, Pc, Pn, dst, sc, tslot); break;
+            case 3: launch_pair_t<false, true, true>(it, s, Pc, Pn, dst, sc, tslot); break;
+            case 4: launch_pair_t<true, false, false>(it, s, Pc, Pn, dst, sc, tslot); break;
+            case 5: launch_pair_t<true, false, true>(it, s, Pc, Pn, dst, sc, tslot); break;
+            case 6: launch_pair_t<true, true, false>(it, s, Pc, Pn, dst, sc, tslot); break;
+            default: launch_pair_t<true, true, true>(it, s, Pc, Pn, dst, sc, tslot); break;
+        }
     }
 
     void mark(int k) {
@@ -519,17 +562,7 @@ struct apbf_gpu_solver {
                 float4* Pn = P[it & 1];
                 const int tslot = kernel_timing ? (int)kt_used++ : -1;
                 if (tslot >= 0) CK(cudaEventRecord(kt_ev[tslot][0], st));
-                KL(k_lambda<<<blocks(n, 256), 256, 0, st>>>(it, ctl, activeCount.p, order.p, Pc, dst.W,
-                                                         dst.L, nbr.p, nbrCount.p, groupBase.p, sc, s));
-                if (tslot >= 0) CK(cudaEventRecord(kt_ev[tslot][1], st));
-                if (cfg.inactive_lambda_zero)
-                    KL(k_deltap_apply<true><<<blocks(n, 256), 256, 0, st>>>(
-                        it, ctl, activeCount.p, order.p, Pc, Pn, dst.W, dst.L, dst.LV, nbr.p, nbrCount.p,
-                        groupBase.p, ws.scene.p, sc, s));
-                else
-                    KL(k_deltap_apply<false><<<blocks(n, 256), 256, 0, st>>>(
-                        it, ctl, activeCount.p, order.p, Pc, Pn, dst.W, dst.L, dst.LV, nbr.p, nbrCount.p,
-                        groupBase.p, ws.scene.p, sc, s));
+                launch_solver_pair(it, s, Pc, Pn, dst, sc, tslot);
                 if (tslot >= 0) CK(cudaEventRecord(kt_ev[tslot][2], st));
                 if (cfg.record_residuals) {
                     CK(cudaMemsetAsync(resid.p + (size_t)s * nMax + (it - 1), 0, sizeof(double), st));
@@ -610,6 +643,8 @@ struct apbf_gpu_solver {
             nbrCap *= 2;
             nbr.release();
             nbr.ensure((size_t)nbrCap);
+            coef.release();
+            coef.ensure((size_t)nbrCap);
         }
         const Ctl& c = *ws.h_ctl;
         if (kernel_timing) collect_kernel_timing(c.total_iterations);
