@@ -12,7 +12,7 @@
 #include <vector>
 #include <array>
 
-#include "apbf_kernels.cuh"
+#include "apbf_tiles.cuh"
 
 using namespace apbf_gpu;
 
@@ -342,6 +342,14 @@ struct apbf_gpu_solver {
     DBuf<int> order, nbrCount, nbr, tileCount, levelCount, activeCount, bucketStart;
     DBuf<long long> groupBase;
     DBuf<float> coef;  // per-list-entry spiky coefficient, lambda -> delta-p
+    // cell-tile solver (apbf_tiles.cuh)
+    DBuf<TileInfo> tileInfo;
+    DBuf<int2> tileRuns;
+    DBuf<int> tileMax, fbLists;
+    DBuf<unsigned short> lists16;
+    DBuf<float> coef16;
+    long long listCap16 = 0, fbCap = 0;
+    int numTilesP = 0;
     DBuf<float4> sortedPM;
     DBuf<float> stage;  // compact host<->device staging (13 words per particle)
     DBuf<double> resid;
@@ -398,6 +406,7 @@ struct apbf_gpu_solver {
         for (auto& e : ev) CK(cudaEventCreate(&e));
         if (const char* v = std::getenv("APBF_STAGE_LISTS")) use_stage = std::atoi(v) != 0;
         if (const char* v = std::getenv("APBF_COEF_CACHE")) use_coef = std::atoi(v) != 0;
+        if (const char* v = std::getenv("APBF_TILES")) use_tiles = std::atoi(v) != 0;
         CK(cudaMemcpy(ws.scene.p, &scene, sizeof(Scene), cudaMemcpyHostToDevice));
         levelCount.ensure(cfg.n_max + 2);
         activeCount.ensure(cfg.n_max + 2);
@@ -427,6 +436,22 @@ struct apbf_gpu_solver {
             coef.ensure((size_t)nbrCap);
         }
         numTiles = (int)((m + kTileSize - 1) / kTileSize);
+        numTilesP = (int)((m + kTileP - 1) / kTileP);
+        tileInfo.ensure(numTilesP);
+        tileRuns.ensure((size_t)numTilesP * kMaxRuns);
+        tileMax.ensure(numTilesP);
+        if (listCap16 < (long long)numTilesP * kTileP * 48) {
+            listCap16 = (long long)numTilesP * kTileP * 48;
+            lists16.release();
+            lists16.ensure((size_t)listCap16);
+            coef16.release();
+            coef16.ensure((size_t)listCap16);
+        }
+        if (fbCap < 64 * 1024) {
+            fbCap = 64 * 1024;
+            fbLists.release();
+            fbLists.ensure((size_t)fbCap);
+        }
         tileCount.ensure((size_t)(cfg.n_max + 1) * numTiles);
         sortedPM.ensure(m);
         stage.ensure(13 * m);
@@ -460,7 +485,7 @@ struct apbf_gpu_solver {
     // slabs in shared memory (bulk async copy); APBF_COEF_CACHE=0 makes the
     // delta-p pass recompute the spiky coefficients instead of reading the
     // lambda pass's cache.  Every variant is bit-identical.
-    bool use_stage = false, use_coef = true;
+    bool use_stage = false, use_coef = true, use_tiles = true;
 
     template <bool kZ, bool kS, bool kC>
     void launch_pair_t(int it, int s, const float4* Pc, float4* Pn, const StateSet& dst,
@@ -478,8 +503,35 @@ struct apbf_gpu_solver {
             groupBase.p, coef.p, ws.scene.p, sc, s));
     }
 
+    template <bool kZ, bool kC>
+    void launch_tile_pair_t(int it, int s, const float4* Pc, float4* Pn, const StateSet& dst,
+                            const SolverConsts& sc, int tslot) {
+        cudaStream_t st = ws.stream;
+        Ctl* ctl = ws.ctl.p;
+        const int smemL = kCandMax * (int)(sizeof(float4) + sizeof(float));
+        const int smemD = kCandMax * (int)sizeof(float4);
+        KL(k_lambda_tile<kC><<<numTilesP, kTileP, smemL, st>>>(n, it, ctl, tileInfo.p, tileRuns.p,
+                                                                tileMax.p, Pc, dst.W, dst.L, dst.LV,
+                                                                lists16.p, fbLists.p, nbrCount.p,
+                                                                coef16.p, sc, s));
+        if (tslot >= 0) CK(cudaEventRecord(kt_ev[tslot][1], st));
+        KL(k_deltap_tile<kZ, kC><<<numTilesP, kTileP, smemD, st>>>(
+            n, it, ctl, tileInfo.p, tileRuns.p, tileMax.p, Pc, Pn, dst.W, dst.L, dst.LV, lists16.p,
+            fbLists.p, nbrCount.p, coef16.p, ws.scene.p, sc, s));
+    }
+
     void launch_solver_pair(int it, int s, const float4* Pc, float4* Pn, const StateSet& dst,
                             const SolverConsts& sc, int tslot) {
+        if (use_tiles) {
+            const int v = (cfg.inactive_lambda_zero ? 2 : 0) | (use_coef ? 1 : 0);
+            switch (v) {
+                case 0: launch_tile_pair_t<false, false>(it, s, Pc, Pn, dst, sc, tslot); break;
+                case 1: launch_tile_pair_t<false, true>(it, s, Pc, Pn, dst, sc, tslot); break;
+                case 2: launch_tile_pair_t<true, false>(it, s, Pc, Pn, dst, sc, tslot); break;
+                default: launch_tile_pair_t<true, true>(it, s, Pc, Pn, dst, sc, tslot); break;
+            }
+            return;
+        }
         const int v = (cfg.inactive_lambda_zero ? 4 : 0) | (use_stage ? 2 : 0) | (use_coef ? 1 : 0);
         switch (v) {
             case 0: launch_pair_t<false, false, false>(it, s, Pc, Pn, dst, sc, tslot); break;
@@ -490,6 +542,30 @@ struct apbf_gpu_solver {
             case 5: launch_pair_t<true, false, true>(it, s, Pc, Pn, dst, sc, tslot); break;
             case 6: launch_pair_t<true, true, false>(it, s, Pc, Pn, dst, sc, tslot); break;
             default: launch_pair_t<true, true, true>(it, s, Pc, Pn, dst, sc, tslot); break;
+        }
+    }
+
+    // After an overflowed list build: grow whichever store ran out.
+    void grow_lists(unsigned long long used, unsigned long long used_fb) {
+        if (!use_tiles) {
+            nbrCap = std::max<long long>(nbrCap * 2, (long long)(used * 3 / 2));
+            nbr.release();
+            nbr.ensure((size_t)nbrCap);
+            coef.release();
+            coef.ensure((size_t)nbrCap);
+            return;
+        }
+        if (used > (unsigned long long)listCap16) {
+            listCap16 = std::max<long long>(listCap16 * 2, (long long)(used * 3 / 2));
+            lists16.release();
+            lists16.ensure((size_t)listCap16);
+            coef16.release();
+            coef16.ensure((size_t)listCap16);
+        }
+        if (used_fb > (unsigned long long)fbCap) {
+            fbCap = std::max<long long>(fbCap * 2, (long long)(used_fb * 3 / 2));
+            fbLists.release();
+            fbLists.ensure((size_t)fbCap);
         }
     }
 
@@ -529,15 +605,25 @@ struct apbf_gpu_solver {
                                                            tileCount.p));
             KL(k_level_scan<<<nMax + 1, 1024, 0, st>>>(ctl, numTiles, tileCount.p, levelCount.p));
             KL(k_level_finish<<<1, 32, 0, st>>>(ctl, n, nMax, levelCount.p, activeCount.p, bucketStart.p));
-            KL(k_level_scatter<<<numTiles, kTileThreads, 9 * smemG, st>>>(n, ctl, dst.LV, nMax, numTiles,
-                                                                     tileCount.p, bucketStart.p, order.p));
-            KL(k_build_lists<<<blocks(n, 256), 256, 0, st>>>(n, ctl, order.p, dst.XS, ws.cellCount.p, cfg.h,
-                                                          cfg.h * cfg.h, nbr.p, nbrCount.p, groupBase.p,
-                                                          nbrCap));
-            if (S > 1)
-                KL(k_prestabilize<<<blocks(n, 256), 256, 0, st>>>(n, ctl, activeCount.p, S, order.p, dst.XS,
-                                                               dst.X, ws.scene.p, radius,
-                                                               cfg.stab_iterations, s));
+            if (use_tiles) {
+                KL(k_tile_build<<<numTilesP, kTileP, 0, st>>>(n, ctl, dst.XS, ws.cellCount.p, dst.LV, cfg.h,
+                                                            cfg.h * cfg.h, tileInfo.p, tileRuns.p, tileMax.p,
+                                                            lists16.p, listCap16, fbLists.p, fbCap,
+                                                            nbrCount.p));
+                if (S > 1)
+                    KL(k_prestabilize_slots<<<blocks(n, 256), 256, 0, st>>>(
+                        n, ctl, S, dst.LV, dst.XS, dst.X, ws.scene.p, radius, cfg.stab_iterations, s));
+            } else {
+                KL(k_level_scatter<<<numTiles, kTileThreads, 9 * smemG, st>>>(
+                    n, ctl, dst.LV, nMax, numTiles, tileCount.p, bucketStart.p, order.p));
+                KL(k_build_lists<<<blocks(n, 256), 256, 0, st>>>(n, ctl, order.p, dst.XS, ws.cellCount.p,
+                                                              cfg.h, cfg.h * cfg.h, nbr.p, nbrCount.p,
+                                                              groupBase.p, nbrCap));
+                if (S > 1)
+                    KL(k_prestabilize<<<blocks(n, 256), 256, 0, st>>>(n, ctl, activeCount.p, S, order.p,
+                                                                   dst.XS, dst.X, ws.scene.p, radius,
+                                                                   cfg.stab_iterations, s));
+            }
             LAUNCH_CHECK();
             mark(2);
             float4* P[2] = {dst.XS, PB.p};
@@ -566,9 +652,14 @@ struct apbf_gpu_solver {
                 if (tslot >= 0) CK(cudaEventRecord(kt_ev[tslot][2], st));
                 if (cfg.record_residuals) {
                     CK(cudaMemsetAsync(resid.p + (size_t)s * nMax + (it - 1), 0, sizeof(double), st));
-                    KL(k_residual<<<blocks(n, 256), 256, 0, st>>>(n, it, ctl, activeCount.p, order.p, Pn,
-                                                               nbr.p, nbrCount.p, groupBase.p, sc,
-                                                               resid.p + (size_t)s * nMax + (it - 1)));
+                    if (use_tiles)
+                        KL(k_residual_tile<<<numTilesP, kTileP, 0, st>>>(
+                            n, it, ctl, activeCount.p, tileInfo.p, tileRuns.p, Pn, lists16.p, fbLists.p,
+                            nbrCount.p, sc, resid.p + (size_t)s * nMax + (it - 1)));
+                    else
+                        KL(k_residual<<<blocks(n, 256), 256, 0, st>>>(n, it, ctl, activeCount.p, order.p, Pn,
+                                                                   nbr.p, nbrCount.p, groupBase.p, sc,
+                                                                   resid.p + (size_t)s * nMax + (it - 1)));
                 }
                 LAUNCH_CHECK();
                 if (observer) {
@@ -640,11 +731,7 @@ struct apbf_gpu_solver {
             if (attempt > 6) fail(APBF_ERR_RUNTIME, "neighbor list overflow");
             cur = start_set;
             copy_set(set[cur], backup);
-            nbrCap *= 2;
-            nbr.release();
-            nbr.ensure((size_t)nbrCap);
-            coef.release();
-            coef.ensure((size_t)nbrCap);
+            grow_lists(ws.h_ctl->list_alloc, ws.h_ctl->list_alloc_fb);
         }
         const Ctl& c = *ws.h_ctl;
         if (kernel_timing) collect_kernel_timing(c.total_iterations);
@@ -955,41 +1042,51 @@ int32_t apbf_gpu_neighbor_lists(int32_t n, const float* positions, float h, floa
         Workspace& ws = component_ws();
         upload_pos4(ws, n, positions);
         component_grid(ws, 0, n, h, padding);
-        // sorted points (the grid's points_ copy) and identity order
-        DBuf<float4> sorted;
-        sorted.ensure(n);
-        DBuf<int> order, cnt, nb;
-        DBuf<long long> gb;
-        order.ensure(n);
-        const size_t groups = ((size_t)n + 31) / 32 + 1;
-        cnt.ensure(groups * 32);
-        gb.ensure(groups);
-        long long cap = (long long)n * 64 + 4096;
+        // sorted points (the grid's points_ copy), then the cell-tile lists
+        // exactly as the solver builds them (apbf_tiles.cuh), decoded to CSR
         cudaStream_t st = ws.stream;
+        const int tiles = (n + kTileP - 1) / kTileP;
+        DBuf<float4> sorted;
+        DBuf<TileInfo> info;
+        DBuf<int2> runs;
+        DBuf<int> tmax, lv, cnt, fb;
+        DBuf<unsigned short> l16;
+        sorted.ensure(n);
+        info.ensure(tiles);
+        runs.ensure((size_t)tiles * kMaxRuns);
+        tmax.ensure(tiles);
+        lv.ensure(n);
+        cnt.ensure(n);
         KL(k_gather_posmass<<<blocks(n, 256), 256, 0, st>>>(n, ws.ctl.p, ws.perm.p, ws.tmp4.p, ws.tmp4.p,
                                                          sorted.p));
-        std::vector<int> iota(n);
-        for (int i = 0; i < n; ++i) iota[i] = i;
-        CK(cudaMemcpyAsync(order.p, iota.data(), sizeof(int) * n, cudaMemcpyHostToDevice, st));
+        CK(cudaMemsetAsync(lv.p, 0, sizeof(int) * n, st));
+        long long cap = (long long)tiles * kTileP * 48, fbcap = 4096;
         for (;;) {
-            nb.release();
-            nb.ensure((size_t)cap);
+            l16.release();
+            l16.ensure((size_t)cap);
+            fb.release();
+            fb.ensure((size_t)fbcap);
+            KL(k_frame_begin<<<1, 1, 0, st>>>(ws.ctl.p));
             KL(k_list_reset<<<1, 1, 0, st>>>(ws.ctl.p));
-            KL(k_build_lists<<<blocks(n, 256), 256, 0, st>>>(n, ws.ctl.p, order.p, sorted.p, ws.cellCount.p,
-                                                          h, h * h, nb.p, cnt.p, gb.p, cap));
+            KL(k_tile_build<<<tiles, kTileP, 0, st>>>(n, ws.ctl.p, sorted.p, ws.cellCount.p, lv.p, h, h * h,
+                                                    info.p, runs.p, tmax.p, l16.p, cap, fb.p, fbcap, cnt.p));
             LAUNCH_CHECK();
             ws.read_ctl();
             if (!ws.h_ctl->list_overflow) break;
-            KL(k_frame_begin<<<1, 1, 0, st>>>(ws.ctl.p));  // clear the abort of the overflowed build
-            cap *= 2;
+            cap = std::max<long long>(cap * 2, (long long)ws.h_ctl->list_alloc * 3 / 2);
+            fbcap = std::max<long long>(fbcap * 2, (long long)ws.h_ctl->list_alloc_fb * 3 / 2);
         }
         std::vector<int> hc(n);
-        std::vector<long long> hg(groups);
-        const long long alloc = (long long)ws.h_ctl->list_alloc;
-        std::vector<int> hn((size_t)std::max<long long>(alloc, 1));
+        std::vector<TileInfo> hi(tiles);
+        std::vector<int2> hr((size_t)tiles * kMaxRuns);
+        const long long used = (long long)ws.h_ctl->list_alloc, usedfb = (long long)ws.h_ctl->list_alloc_fb;
+        std::vector<unsigned short> h16((size_t)std::max<long long>(used, 1));
+        std::vector<int> hfb((size_t)std::max<long long>(usedfb, 1));
         CK(cudaMemcpy(hc.data(), cnt.p, sizeof(int) * n, cudaMemcpyDeviceToHost));
-        CK(cudaMemcpy(hg.data(), gb.p, sizeof(long long) * groups, cudaMemcpyDeviceToHost));
-        if (alloc > 0) CK(cudaMemcpy(hn.data(), nb.p, sizeof(int) * alloc, cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(hi.data(), info.p, sizeof(TileInfo) * tiles, cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(hr.data(), runs.p, sizeof(int2) * hr.size(), cudaMemcpyDeviceToHost));
+        if (used > 0) CK(cudaMemcpy(h16.data(), l16.p, sizeof(unsigned short) * used, cudaMemcpyDeviceToHost));
+        if (usedfb > 0) CK(cudaMemcpy(hfb.data(), fb.p, sizeof(int) * usedfb, cudaMemcpyDeviceToHost));
         long long total = 0;
         for (int i = 0; i < n; ++i) total += hc[i];
         if (total_out) *total_out = total;
@@ -1000,8 +1097,22 @@ int32_t apbf_gpu_neighbor_lists(int32_t n, const float* positions, float h, floa
         if (indices) {
             if (indices_capacity < total) fail(APBF_ERR_INVALID_ARGUMENT, "indices capacity too small");
             long long w = 0;
-            for (int i = 0; i < n; ++i)
-                for (int e = 0; e < hc[i]; ++e) indices[w++] = hn[hg[i >> 5] + (long long)e * 32 + (i & 31)];
+            for (int i = 0; i < n; ++i) {
+                const int t = i / kTileP, p = i % kTileP;
+                const TileInfo& ti = hi[t];
+                const long long off = (long long)ti.listBase + (long long)p * ti.cap;
+                for (int e = 0; e < hc[i]; ++e) {
+                    if (ti.C < 0) {
+                        indices[w++] = hfb[off + e];
+                    } else {
+                        const int c = h16[off + e];
+                        int r = 0;
+                        while (r + 1 < ti.nRuns && hr[(size_t)t * kMaxRuns + r + 1].y <= c) ++r;
+                        const int2 run = hr[(size_t)t * kMaxRuns + r];
+                        indices[w++] = run.x + (c - run.y);
+                    }
+                }
+            }
         }
     });
 }
