@@ -407,6 +407,9 @@ struct apbf_gpu_solver {
         if (const char* v = std::getenv("APBF_STAGE_LISTS")) use_stage = std::atoi(v) != 0;
         if (const char* v = std::getenv("APBF_COEF_CACHE")) use_coef = std::atoi(v) != 0;
         if (const char* v = std::getenv("APBF_TILES")) use_tiles = std::atoi(v) != 0;
+        if (const char* v = std::getenv("APBF_BLOCK")) block_threads = std::atoi(v);
+        if (block_threads != 256 && block_threads != 512 && block_threads != 1024) block_threads = 128;
+        configure_carveouts();
         CK(cudaMemcpy(ws.scene.p, &scene, sizeof(Scene), cudaMemcpyHostToDevice));
         levelCount.ensure(cfg.n_max + 2);
         activeCount.ensure(cfg.n_max + 2);
@@ -485,22 +488,56 @@ struct apbf_gpu_solver {
     // slabs in shared memory (bulk async copy); APBF_COEF_CACHE=0 makes the
     // delta-p pass recompute the spiky coefficients instead of reading the
     // lambda pass's cache.  Every variant is bit-identical.
-    bool use_stage = false, use_coef = true, use_tiles = true;
+    bool use_stage = false, use_coef = true, use_tiles = false;
+    int block_threads = 128;  // APBF_BLOCK: CTA size of the order-based passes
+
+    template <bool kZ, bool kS, bool kC, int kBT>
+    void launch_pair_bt(int it, int s, const float4* Pc, float4* Pn, const StateSet& dst,
+                        const SolverConsts& sc, int tslot) {
+        cudaStream_t st = ws.stream;
+        Ctl* ctl = ws.ctl.p;
+        const int sb = blocks(n, kBT);
+        const int smem = kS ? kSolverSmem : 0;
+        KL(k_lambda<kS, kC, kBT><<<sb, kBT, smem, st>>>(n, it, ctl, activeCount.p, order.p, Pc, dst.W,
+                                                         dst.L, nbr.p, nbrCount.p, groupBase.p, coef.p,
+                                                         sc, s));
+        if (tslot >= 0) CK(cudaEventRecord(kt_ev[tslot][1], st));
+        KL(k_deltap_apply<kZ, kS, kC, kBT><<<sb, kBT, smem, st>>>(
+            n, it, ctl, activeCount.p, order.p, Pc, Pn, dst.W, dst.L, dst.LV, nbr.p, nbrCount.p,
+            groupBase.p, coef.p, ws.scene.p, sc, s));
+    }
 
     template <bool kZ, bool kS, bool kC>
     void launch_pair_t(int it, int s, const float4* Pc, float4* Pn, const StateSet& dst,
                        const SolverConsts& sc, int tslot) {
-        cudaStream_t st = ws.stream;
-        Ctl* ctl = ws.ctl.p;
-        const int sb = blocks(n, kSolverThreads);
-        const int smem = kS ? kSolverSmem : 0;
-        KL(k_lambda<kS, kC><<<sb, kSolverThreads, smem, st>>>(n, it, ctl, activeCount.p, order.p, Pc,
-                                                               dst.W, dst.L, nbr.p, nbrCount.p,
-                                                               groupBase.p, coef.p, sc, s));
-        if (tslot >= 0) CK(cudaEventRecord(kt_ev[tslot][1], st));
-        KL(k_deltap_apply<kZ, kS, kC><<<sb, kSolverThreads, smem, st>>>(
-            n, it, ctl, activeCount.p, order.p, Pc, Pn, dst.W, dst.L, dst.LV, nbr.p, nbrCount.p,
-            groupBase.p, coef.p, ws.scene.p, sc, s));
+        if (kS || block_threads == 128) launch_pair_bt<kZ, kS, kC, 128>(it, s, Pc, Pn, dst, sc, tslot);
+        else if (block_threads == 256) launch_pair_bt<kZ, kS, kC, 256>(it, s, Pc, Pn, dst, sc, tslot);
+        else if (block_threads == 512) launch_pair_bt<kZ, kS, kC, 512>(it, s, Pc, Pn, dst, sc, tslot);
+        else launch_pair_bt<kZ, kS, kC, 1024>(it, s, Pc, Pn, dst, sc, tslot);
+    }
+
+    // The gather passes want L1, not shared memory (they use none unless
+    // list staging is on).
+    template <int kBT>
+    static void carveout_bt() {
+        const int a = cudaSharedmemCarveoutMaxL1;
+        cudaFuncSetAttribute(k_lambda<false, true, kBT>, cudaFuncAttributePreferredSharedMemoryCarveout, a);
+        cudaFuncSetAttribute(k_lambda<false, false, kBT>, cudaFuncAttributePreferredSharedMemoryCarveout, a);
+        cudaFuncSetAttribute(k_deltap_apply<false, false, true, kBT>,
+                             cudaFuncAttributePreferredSharedMemoryCarveout, a);
+        cudaFuncSetAttribute(k_deltap_apply<false, false, false, kBT>,
+                             cudaFuncAttributePreferredSharedMemoryCarveout, a);
+        cudaFuncSetAttribute(k_deltap_apply<true, false, true, kBT>,
+                             cudaFuncAttributePreferredSharedMemoryCarveout, a);
+        cudaFuncSetAttribute(k_deltap_apply<true, false, false, kBT>,
+                             cudaFuncAttributePreferredSharedMemoryCarveout, a);
+    }
+    void configure_carveouts() {
+        carveout_bt<128>();
+        carveout_bt<256>();
+        carveout_bt<512>();
+        carveout_bt<1024>();
+        cudaGetLastError();
     }
 
     template <bool kZ, bool kC>
