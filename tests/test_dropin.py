@@ -1,0 +1,26 @@
+"""The C++ drop-in (include/apbf_gpu/solver.hpp) compiled against the
+reference's own headers (oracle/_ref/dropin_demo, built by oracle/Makefile)."""
+import os
+import subprocess
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+DEMO = os.path.join(ROOT, "oracle", "_ref", "dropin_demo")
+
+
+@pytest.mark.ref
+def test_dropin_compiles_against_reference_headers():
+    if not os.path.isdir("/root/reference/proj"):
+        pytest.skip("reference sources not present")
+    subprocess.run(["make", "-s", "-C", os.path.join(ROOT, "oracle"), "ref"], check=True)
+    assert os.access(DEMO, os.X_OK)
+
+
+@pytest.mark.gpu
+@pytest.mark.skipif(not os.path.exists(DEMO), reason="oracle/_ref/dropin_demo not built")
+@pytest.mark.parametrize("scenario,scale", [("multi_dam_break", "0.05"), ("dam_break", "0.03")])
+def test_dropin_matches_reference_solver_bitwise(scenario, scale):
+    out = subprocess.run([DEMO, scenario, scale, "4"], capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stdout + out.stderr
+    assert "DROPIN OK" in out.stdout
