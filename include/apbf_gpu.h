@@ -200,6 +200,51 @@ uint64_t apbf_gpu_launch_count(void);
 int32_t apbf_gpu_last_neighbor_stats(const apbf_gpu_solver* s, int64_t* total_entries,
                                      int64_t* list_capacity);
 
+/* ---- z-slab domain decomposition ----
+ * The reference has no distributed code; these entry points run the same
+ * stepFrame over G ranks that own z-slabs of the substep's global grid,
+ * with migration + 2-layer halos exchanged as particle records and one x*
+ * halo exchange per solver iteration.  Results equal the single-GPU run bit
+ * for bit.  Global storage order = rank 0's owned particles, then rank 1's,
+ * ... (set_state splits the caller's arrays into contiguous ranges). */
+typedef struct apbf_gpu_group apbf_gpu_group;
+
+/* G ranks in this process (host thread per rank); devices[r] is rank r's
+ * GPU (NULL: all on device 0 -- the single-GPU test mode). */
+int32_t apbf_gpu_group_create(const apbf_solver_config* cfg, const apbf_sdf_primitive* prims,
+                              int32_t n_prims, float gradient_step, int32_t nranks,
+                              const int32_t* devices, apbf_gpu_group** out, apbf_error* err);
+void apbf_gpu_group_destroy(apbf_gpu_group* g);
+int32_t apbf_gpu_group_size(const apbf_gpu_group* g);
+int32_t apbf_gpu_group_set_state(apbf_gpu_group* g, int32_t n, const float* x, const float* x_star,
+                                 const float* v, const float* mass, const float* inv_mass,
+                                 const float* lambda, const int32_t* level, apbf_error* err);
+int32_t apbf_gpu_group_get_state(apbf_gpu_group* g, float* x, float* x_star, float* v, float* mass,
+                                 float* inv_mass, float* lambda, int32_t* level, apbf_error* err);
+int32_t apbf_gpu_group_particle_counts(const apbf_gpu_group* g, int32_t* counts);
+int32_t apbf_gpu_group_step_frame(apbf_gpu_group* g, const apbf_camera* cam,
+                                  const apbf_lod_config* lod, int32_t frame_index,
+                                  apbf_frame_stats* out, apbf_error* err);
+int32_t apbf_gpu_group_step_frame_with_levels(apbf_gpu_group* g, int32_t frame_index,
+                                              apbf_frame_stats* out, apbf_error* err);
+
+/* One process per GPU: rank r of nranks joins an NCCL communicator (unique
+ * id from rank 0, broadcast by the caller), then uploads its contiguous
+ * slice of the global state with apbf_gpu_slab_set_state; step_frame /
+ * get_state then act on this rank's owned particles. */
+int32_t apbf_gpu_nccl_unique_id(uint8_t* id128, apbf_error* err);
+int32_t apbf_gpu_solver_attach_nccl(apbf_gpu_solver* s, int32_t rank, int32_t nranks,
+                                    const uint8_t* id128, apbf_error* err);
+int32_t apbf_gpu_slab_set_state(apbf_gpu_solver* s, int32_t n_local, int64_t n_global,
+                                const float* x, const float* x_star, const float* v,
+                                const float* mass, const float* inv_mass, const float* lambda,
+                                const int32_t* level, apbf_error* err);
+
+/* Host logic of the decomposition (no GPU needed): equal-count partition of
+ * a per-layer particle histogram into nranks slabs of >= min_layers layers. */
+int32_t apbf_slab_partition(const int64_t* layer_hist, int32_t layers, int32_t nranks,
+                            int32_t min_layers, int32_t* zlo, int32_t* zhi);
+
 /* ---- component entry points (reference free functions / classes) ---- */
 
 /* UniformGrid<float>::build (uniform_grid.hpp:42-98).  perm: n ints;

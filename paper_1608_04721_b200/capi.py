@@ -97,6 +97,26 @@ SIGNATURES = {
     "apbf_gpu_kernel_times": (C.c_int32, [C.c_void_p, C.POINTER(C.c_double),
                                           C.POINTER(C.c_double), _lp, _lp]),
     "apbf_gpu_launch_count": (C.c_uint64, []),
+    "apbf_gpu_group_create": (C.c_int32, [C.POINTER(apbf_solver_config),
+                                          C.POINTER(apbf_sdf_primitive), C.c_int32, C.c_float,
+                                          C.c_int32, _ip, C.POINTER(C.c_void_p), _ep]),
+    "apbf_gpu_group_destroy": (None, [C.c_void_p]),
+    "apbf_gpu_group_size": (C.c_int32, [C.c_void_p]),
+    "apbf_gpu_group_set_state": (C.c_int32, [C.c_void_p, C.c_int32, _fp, _fp, _fp, _fp, _fp, _fp,
+                                             _ip, _ep]),
+    "apbf_gpu_group_get_state": (C.c_int32, [C.c_void_p, _fp, _fp, _fp, _fp, _fp, _fp, _ip, _ep]),
+    "apbf_gpu_group_particle_counts": (C.c_int32, [C.c_void_p, _ip]),
+    "apbf_gpu_group_step_frame": (C.c_int32, [C.c_void_p, C.POINTER(apbf_camera),
+                                              C.POINTER(apbf_lod_config), C.c_int32,
+                                              C.POINTER(apbf_frame_stats), _ep]),
+    "apbf_gpu_group_step_frame_with_levels": (C.c_int32, [C.c_void_p, C.c_int32,
+                                                          C.POINTER(apbf_frame_stats), _ep]),
+    "apbf_gpu_nccl_unique_id": (C.c_int32, [C.POINTER(C.c_uint8), _ep]),
+    "apbf_gpu_solver_attach_nccl": (C.c_int32, [C.c_void_p, C.c_int32, C.c_int32,
+                                                C.POINTER(C.c_uint8), _ep]),
+    "apbf_gpu_slab_set_state": (C.c_int32, [C.c_void_p, C.c_int32, C.c_int64, _fp, _fp, _fp, _fp,
+                                            _fp, _fp, _ip, _ep]),
+    "apbf_slab_partition": (C.c_int32, [_lp, C.c_int32, C.c_int32, C.c_int32, _ip, _ip]),
     "apbf_gpu_grid_build": (C.c_int32, [C.c_int32, _fp, C.c_float, C.c_float, _ip, _fp, _ip, _ip,
                                         C.c_int64, _lp, _ep]),
     "apbf_gpu_neighbor_lists": (C.c_int32, [C.c_int32, _fp, C.c_float, C.c_float, _ip, _ip,

@@ -1,0 +1,321 @@
+// apbf_dist.cuh -- kernels of the z-slab domain decomposition.
+//
+// Rank g owns the particles whose cell layer cz (of the substep's GLOBAL
+// grid) lies in [zlo_g, zhi_g).  Every substep each rank sends every other
+// rank q -- in its current (previous global) storage order -- the particles
+// whose cz falls in q's slab extended by the 2-layer halo; q concatenates
+// what it receives in source-rank order (its own particles in place g) and
+// stable-sorts by cell, which reproduces the single-GPU global order
+// restricted to its extended range.  Owned particles are then contiguous,
+// lower ghosts precede them and upper ghosts follow, so every neighbour list
+// and every per-particle sum is the single-GPU one, bit for bit.
+#pragma once
+
+#include "apbf_kernels.cuh"
+
+namespace apbf_gpu {
+
+constexpr int kMaxRanks = 32;
+
+__device__ __forceinline__ int layer_of(const GridDev& G, float h, float z) {
+    const int v = f2i_trunc(floorf((z - G.origin[2]) / h));
+    return imin_std(imax_std(v, 0), G.dims[2] - 1);
+}
+
+// Particles per cz layer (global grid g) -> hist[dims.z].
+__global__ void k_layer_hist(int n, const float4* __restrict__ P, const Ctl* ctl, int g, float h,
+                             int* __restrict__ hist) {
+    if (ctl->abort) return;
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) atomicAdd(&hist[layer_of(ctl->grid[g], h, P[i].z)], 1);
+}
+
+// Destination bit mask: bit q set when cz in [lo[q] - halo, hi[q] + halo).
+__global__ void k_dest_mask(int n, const float4* __restrict__ P, const Ctl* ctl, int g, float h,
+                            const int* __restrict__ lo, const int* __restrict__ hi, int G, int halo,
+                            unsigned* __restrict__ mask) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int cz = layer_of(ctl->grid[g], h, P[i].z);
+    unsigned m = 0;
+    for (int q = 0; q < G; ++q)
+        if (cz >= lo[q] - halo && cz < hi[q] + halo) m |= 1u << q;
+    mask[i] = m;
+}
+
+// Stable expansion by destination: per tile (kTileSize elements) counts of
+// every destination bit, column-major tileCount[q * numTiles + tile].
+__global__ void __launch_bounds__(kTileThreads) k_mask_tile_counts(int n, const unsigned* __restrict__ mask,
+                                                                   int G, int numTiles,
+                                                                   int* __restrict__ tileCount) {
+    __shared__ int s_c[kMaxRanks];
+    for (int q = threadIdx.x; q < G; q += blockDim.x) s_c[q] = 0;
+    __syncthreads();
+    const int tile = blockIdx.x;
+    for (int r = 0; r < kTileRounds; ++r) {
+        const int k = tile * kTileSize + r * kTileThreads + threadIdx.x;
+        const unsigned m = k < n ? mask[k] : 0u;
+        for (int q = 0; q < G; ++q) {
+            const unsigned b = __ballot_sync(0xffffffffu, (m >> q) & 1u);
+            if ((threadIdx.x & 31) == 0 && b) atomicAdd(&s_c[q], __popc(b));
+        }
+    }
+    __syncthreads();
+    for (int q = threadIdx.x; q < G; q += blockDim.x) tileCount[(long long)q * numTiles + tile] = s_c[q];
+}
+
+// outIdx[destStart[q] + tileOffset[q][tile] + rank] = k, rank = number of
+// earlier elements of the tile with bit q (order preserving).
+__global__ void __launch_bounds__(kTileThreads) k_mask_scatter(int n, const unsigned* __restrict__ mask,
+                                                               int G, int numTiles,
+                                                               const int* __restrict__ tileOffset,
+                                                               const int* __restrict__ destStart,
+                                                               int* __restrict__ outIdx) {
+    __shared__ int s_run[kMaxRanks];
+    __shared__ int s_wc[kTileThreads / 32][kMaxRanks];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int tile = blockIdx.x;
+    for (int q = threadIdx.x; q < G; q += blockDim.x) s_run[q] = 0;
+    __syncthreads();
+    for (int r = 0; r < kTileRounds; ++r) {
+        const int k = tile * kTileSize + r * kTileThreads + threadIdx.x;
+        const unsigned m = k < n ? mask[k] : 0u;
+        for (int q = 0; q < G; ++q) {
+            const unsigned b = __ballot_sync(0xffffffffu, (m >> q) & 1u);
+            if (lane == 0) s_wc[warp][q] = __popc(b);
+        }
+        __syncthreads();
+        for (int q = 0; q < G; ++q) {
+            const unsigned b = __ballot_sync(0xffffffffu, (m >> q) & 1u);
+            if ((m >> q) & 1u) {
+                int before = s_run[q] + __popc(b & ((1u << lane) - 1u));
+                for (int w = 0; w < warp; ++w) before += s_wc[w][q];
+                outIdx[destStart[q] + tileOffset[(long long)q * numTiles + tile] + before] = k;
+            }
+        }
+        __syncthreads();
+        for (int q = threadIdx.x; q < G; q += blockDim.x) {
+            int s = 0;
+            for (int w = 0; w < kTileThreads / 32; ++w) s += s_wc[w][q];
+            s_run[q] += s;
+        }
+        __syncthreads();
+    }
+}
+
+// Exclusive scan of tileCount[q][*] per destination q (one block each).
+__global__ void __launch_bounds__(1024) k_mask_scan(int numTiles, int* __restrict__ tileCount,
+                                                    int* __restrict__ destCount) {
+    const int q = blockIdx.x;
+    int* row = tileCount + (long long)q * numTiles;
+    __shared__ int s_w[32];
+    __shared__ int s_carry;
+    if (threadIdx.x == 0) s_carry = 0;
+    __syncthreads();
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int t0 = 0; t0 < numTiles; t0 += blockDim.x) {
+        const int t = t0 + threadIdx.x;
+        const int v = t < numTiles ? row[t] : 0;
+        int incl = v;
+        for (int o = 1; o < 32; o <<= 1) {
+            const int x = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += x;
+        }
+        if (lane == 31) s_w[warp] = incl;
+        __syncthreads();
+        if (warp == 0) {
+            int w = s_w[lane];
+            int wi = w;
+            for (int o = 1; o < 32; o <<= 1) {
+                const int x = __shfl_up_sync(0xffffffffu, wi, o);
+                if (lane >= o) wi += x;
+            }
+            s_w[lane] = wi - w;
+        }
+        __syncthreads();
+        const int excl = s_carry + s_w[warp] + incl - v;
+        if (t < numTiles) row[t] = excl;
+        __syncthreads();
+        if (threadIdx.x == blockDim.x - 1) s_carry = excl + v;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) destCount[q] = s_carry;
+}
+
+// 16-word particle record for the all-to-all: x(3) v(3) x*(3) mass invMass
+// lambda level pad(3).
+struct alignas(64) Rec {
+    float x[3], v[3], xs[3], m, w, lam;
+    int lv;
+    int pad[3];
+};
+
+__global__ void k_pack_recs(int cnt, const int* __restrict__ idx, StateSet s, Rec* __restrict__ out) {
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= cnt) return;
+    const int i = idx[k];
+    const float4 x = s.X[i], v = s.V[i], xs = s.XS[i];
+    Rec r;
+    r.x[0] = x.x;
+    r.x[1] = x.y;
+    r.x[2] = x.z;
+    r.v[0] = v.x;
+    r.v[1] = v.y;
+    r.v[2] = v.z;
+    r.xs[0] = xs.x;
+    r.xs[1] = xs.y;
+    r.xs[2] = xs.z;
+    r.m = xs.w;
+    r.w = s.W[i];
+    r.lam = s.L[i];
+    r.lv = s.LV[i];
+    r.pad[0] = r.pad[1] = r.pad[2] = 0;
+    out[k] = r;
+}
+
+__global__ void k_unpack_recs(int cnt, const Rec* __restrict__ in, StateSet d) {
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= cnt) return;
+    const Rec r = in[k];
+    d.X[k] = make_float4(r.x[0], r.x[1], r.x[2], 0.f);
+    d.V[k] = make_float4(r.v[0], r.v[1], r.v[2], 0.f);
+    d.XS[k] = make_float4(r.xs[0], r.xs[1], r.xs[2], r.m);
+    d.W[k] = r.w;
+    d.L[k] = r.lam;
+    d.LV[k] = r.lv;
+}
+
+// Slot boundaries of the slab after the local sort: start of layer z is
+// cellStart[z * dx * dy] (z clamped to [0, dz]).  out = {ownBegin, ownEnd,
+// l1Begin, l1End, lowSendEnd, highSendBegin}.
+__global__ void k_slab_bounds(const Ctl* ctl, const int* __restrict__ cellStart, int zlo, int zhi,
+                              int* __restrict__ out) {
+    const GridDev& G = ctl->grid[0];
+    const long long layer = (long long)G.dims[0] * G.dims[1];
+    auto start = [&](int z) {
+        z = imin_std(imax_std(z, 0), G.dims[2]);
+        return cellStart[(long long)z * layer];
+    };
+    out[0] = start(zlo);
+    out[1] = start(zhi);
+    out[2] = start(zlo - 1);
+    out[3] = start(zhi + 1);
+    out[4] = start(zlo + 2);
+    out[5] = start(zhi - 2);
+}
+
+// Levels seen by the iteration order: 0 (never active) outside [b, e).
+__global__ void k_mask_levels(int n, const int* __restrict__ LV, int b, int e, int* __restrict__ out) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) out[i] = (i >= b && i < e) ? LV[i] : 0;
+}
+
+// Per-tile level histogram (the part of k_gather the slab path needs on the
+// masked levels).
+__global__ void __launch_bounds__(kTileThreads) k_level_tiles(int n, const Ctl* ctl, const int* __restrict__ LV,
+                                                              int nMax, int numTiles,
+                                                              int* __restrict__ tileCount) {
+    if (ctl->abort) return;
+    extern __shared__ int s_cnt[];
+    for (int l = threadIdx.x; l <= nMax; l += blockDim.x) s_cnt[l] = 0;
+    __syncthreads();
+    for (int r = 0; r < kTileRounds; ++r) {
+        const int k = blockIdx.x * kTileSize + r * kTileThreads + threadIdx.x;
+        if (k < n) atomicAdd(&s_cnt[imin_std(imax_std(LV[k], 0), nMax)], 1);
+    }
+    __syncthreads();
+    for (int l = threadIdx.x; l <= nMax; l += blockDim.x)
+        tileCount[(long long)l * numTiles + blockIdx.x] = s_cnt[l];
+}
+
+// sum of levels over [b, e) (the owned particles' particle-iterations).
+__global__ void k_level_sum(int b, int e, const int* __restrict__ LV, Ctl* ctl) {
+    const int i = b + blockIdx.x * blockDim.x + threadIdx.x;
+    int v = i < e ? LV[i] : 0;
+    v = warp_sum_i(v);
+    if ((threadIdx.x & 31) == 0 && v) atomicAdd(&ctl->total_iterations, (unsigned long long)v);
+}
+
+// Metrics ghost records: (x, y, z, mass) + owned flag in the w of a second
+// float? -- packed as float4 xyzm and an int flag array.
+__global__ void k_pack_pm(int cnt, const int* __restrict__ idx, const float4* __restrict__ X,
+                          const float4* __restrict__ XS, float4* __restrict__ out) {
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= cnt) return;
+    const int i = idx[k];
+    const float4 x = X[i];
+    out[k] = make_float4(x.x, x.y, x.z, XS[i].w);
+}
+
+// Densities of the owned particles of a sorted (position, mass) array whose
+// owned flags travelled through the same permutation.
+__global__ void k_density_stats_owned(int n, Ctl* ctl, const float4* __restrict__ S,
+                                      const int* __restrict__ owned, const int* __restrict__ cellStart,
+                                      KernelConsts kc) {
+    if (ctl->abort) return;
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    const GridDev& G = ctl->grid[1];
+    float rho = 0.f;
+    const bool valid = k < n && owned[k];
+    if (valid) {
+        const float4 q = S[k];
+        const float p[3] = {q.x, q.y, q.z};
+        int lo[3], hi[3];
+        bool any = true;
+        for (int a = 0; a < 3; ++a) {
+            const int c = f2i_trunc(floorf((p[a] - G.origin[a]) / kc.h));
+            lo[a] = imax_std(c - 1, 0);
+            hi[a] = imin_std(c + 1, G.dims[a] - 1);
+            if (lo[a] > hi[a]) any = false;
+        }
+        if (any) {
+            for (int cz = lo[2]; cz <= hi[2]; ++cz)
+                for (int cy = lo[1]; cy <= hi[1]; ++cy) {
+                    const long long rowBase = ((long long)cz * G.dims[1] + cy) * G.dims[0];
+                    const int b = cellStart[rowBase + lo[0]];
+                    const int e = cellStart[rowBase + hi[0] + 1];
+                    for (int j = b; j < e; ++j) {
+                        const float4 pj = S[j];
+                        const float r2 = sqn3(q.x - pj.x, q.y - pj.y, q.z - pj.z);
+                        if (r2 < kc.h2) rho += pj.w * poly6_r2(kc, r2);
+                    }
+                }
+        }
+    }
+    double s = valid ? (double)rho : 0.0;
+    int mn = valid ? f2ord(rho) : 0x7fffffff;
+    int mx = valid ? f2ord(rho) : (int)0x80000000;
+    for (int o = 16; o > 0; o >>= 1) {
+        s += __shfl_xor_sync(0xffffffffu, s, o);
+        mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+        mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicAdd(&ctl->rho_sum, s);
+        atomicMin(&ctl->rho_min_ord, mn);
+        atomicMax(&ctl->rho_max_ord, mx);
+    }
+}
+
+// gather of an int array through a permutation (owned flags of the metrics sort)
+__global__ void k_gather_int(int n, const int* __restrict__ perm, const int* __restrict__ in,
+                             int* __restrict__ out) {
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k < n) out[k] = in[perm[k]];
+}
+
+// metrics-grid cz range of the owned particles (positions X) -> minmax[2]
+__global__ void k_layer_minmax(int n, const float4* __restrict__ X, const Ctl* ctl, int g, float h,
+                               int* __restrict__ minmax) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    int lo = 0x7fffffff, hi = (int)0x80000000;
+    if (i < n) lo = hi = layer_of(ctl->grid[g], h, X[i].z);
+    lo = warp_min_i(lo);
+    hi = warp_max_i(hi);
+    if ((threadIdx.x & 31) == 0) {
+        atomicMin(&minmax[0], lo);
+        atomicMax(&minmax[1], hi);
+    }
+}
+
+}  // namespace apbf_gpu

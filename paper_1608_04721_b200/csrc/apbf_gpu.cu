@@ -13,6 +13,12 @@
 #include <array>
 
 #include "apbf_tiles.cuh"
+#include "apbf_dist.cuh"
+#include "apbf_transport.h"
+
+#include <memory>
+#include <functional>
+#include <thread>
 
 using namespace apbf_gpu;
 
@@ -490,6 +496,7 @@ struct apbf_gpu_solver {
     // lambda pass's cache.  Every variant is bit-identical.
     bool use_stage = false, use_coef = true, use_tiles = false;
     int block_threads = 128;  // APBF_BLOCK: CTA size of the order-based passes
+    int ownB_ = 0, ownE_ = 0x7fffffff;  // owned slot range (slab mode); everything otherwise
 
     template <bool kZ, bool kS, bool kC, int kBT>
     void launch_pair_bt(int it, int s, const float4* Pc, float4* Pn, const StateSet& dst,
@@ -500,11 +507,11 @@ struct apbf_gpu_solver {
         const int smem = kS ? kSolverSmem : 0;
         KL(k_lambda<kS, kC, kBT><<<sb, kBT, smem, st>>>(n, it, ctl, activeCount.p, order.p, Pc, dst.W,
                                                          dst.L, nbr.p, nbrCount.p, groupBase.p, coef.p,
-                                                         sc, s));
+                                                         sc, s, ownB_, ownE_));
         if (tslot >= 0) CK(cudaEventRecord(kt_ev[tslot][1], st));
         KL(k_deltap_apply<kZ, kS, kC, kBT><<<sb, kBT, smem, st>>>(
             n, it, ctl, activeCount.p, order.p, Pc, Pn, dst.W, dst.L, dst.LV, nbr.p, nbrCount.p,
-            groupBase.p, coef.p, ws.scene.p, sc, s));
+            groupBase.p, coef.p, ws.scene.p, sc, s, ownB_, ownE_));
     }
 
     template <bool kZ, bool kS, bool kC>
@@ -737,6 +744,10 @@ struct apbf_gpu_solver {
     void frame(bool assign_lod, const apbf_camera* cam, const apbf_lod_config* lod, int frame_index,
                apbf_frame_stats* out) {
         CK(cudaSetDevice(ws.device));
+        if (transport) {
+            frame_dist(assign_lod, cam, lod, frame_index, out);
+            return;
+        }
         if (assign_lod && cfg.mode == APBF_MODE_APBF) {
             apbf_lod_config lc = *lod;
             validate_lod(lc);
@@ -832,6 +843,500 @@ struct apbf_gpu_solver {
             double* r = out->residuals;
             int rc = out->residuals_capacity;
             *out = st;
+            out->residuals = r;
+            out->residuals_capacity = rc;
+        }
+    }
+
+    // ================================================ z-slab decomposition
+    // (kernels in apbf_dist.cuh).  Active when `transport` is
+    // set: this handle is rank g of G and holds only its owned particles.
+
+    Transport* transport = nullptr;
+    std::unique_ptr<Transport> transport_owned;
+    long long n_capacity = 0;
+    DBuf<int> layerHist, zRange, bounds, destTile, destCountD, destStartD, sendIdx, LVo, ownedFlag,
+        ownedSorted, minmax;
+    DBuf<unsigned> destMask;
+    DBuf<Rec> sendRec, recvRec;
+    DBuf<float4> sendPM, recvPM;
+    std::vector<long long> prefixPre, prefixPost;
+    bool slab_error = false;
+
+    static long long prefix_of(const std::vector<long long>& c, int g) {
+        long long p = 0;
+        for (int q = 0; q < g; ++q) p += c[q];
+        return p;
+    }
+
+    std::vector<long long> all_counts(Transport& T, long long mine) {
+        std::vector<long long> snd(T.size(), mine), rcv(T.size());
+        T.alltoall_counts(snd.data(), rcv.data());
+        rcv[T.rank()] = mine;
+        return rcv;
+    }
+
+    // Upload this rank's slice (the rank's contiguous part of the global
+    // storage order) with buffers sized for the global particle count.
+    void set_state_local(int nloc, long long ntotal, const float* x, const float* xs, const float* v,
+                         const float* mass, const float* inv_mass, const float* lambda,
+                         const int32_t* level) {
+        allocate((int)std::max<long long>(ntotal, 1));
+        n_capacity = std::max<long long>(ntotal, 1);
+        destMask.ensure(n_capacity);
+        sendIdx.ensure(n_capacity);
+        LVo.ensure(n_capacity);
+        ownedFlag.ensure(n_capacity);
+        ownedSorted.ensure(n_capacity);
+        sendRec.ensure(n_capacity);
+        recvRec.ensure(n_capacity);
+        sendPM.ensure(n_capacity);
+        recvPM.ensure(n_capacity);
+        zRange.ensure(2 * kMaxRanks);
+        bounds.ensure(8);
+        destCountD.ensure(kMaxRanks);
+        destStartD.ensure(kMaxRanks);
+        minmax.ensure(2);
+        n = nloc;
+        cur = 0;
+        levels_valid = true;
+        for (int i = 0; i < nloc; ++i)
+            levels_valid = levels_valid && level[i] >= cfg.n_min && level[i] <= cfg.n_max;
+        if (nloc == 0) return;
+        cudaStream_t st = ws.stream;
+        float* d = stage.p;
+        const size_t n1 = sizeof(float) * (size_t)nloc, n3 = 3 * n1;
+        CK(cudaMemcpyAsync(d, x, n3, cudaMemcpyHostToDevice, st));
+        CK(cudaMemcpyAsync(d + 3LL * nloc, xs, n3, cudaMemcpyHostToDevice, st));
+        CK(cudaMemcpyAsync(d + 6LL * nloc, v, n3, cudaMemcpyHostToDevice, st));
+        CK(cudaMemcpyAsync(d + 9LL * nloc, mass, n1, cudaMemcpyHostToDevice, st));
+        CK(cudaMemcpyAsync(d + 10LL * nloc, inv_mass, n1, cudaMemcpyHostToDevice, st));
+        CK(cudaMemcpyAsync(d + 11LL * nloc, lambda, n1, cudaMemcpyHostToDevice, st));
+        CK(cudaMemcpyAsync(d + 12LL * nloc, level, n1, cudaMemcpyHostToDevice, st));
+        KL(k_unpack_state<<<blocks(nloc, 256), 256, 0, st>>>(nloc, d, set[0].view()));
+        LAUNCH_CHECK();
+        CK(cudaStreamSynchronize(st));
+    }
+
+    // Stable expansion of the `n` current particles by destination mask:
+    // returns per-destination counts and fills sendIdx (grouped by dest).
+    void expand_by_dest(int nn, int G, std::vector<long long>& cnt, std::vector<long long>& start) {
+        cudaStream_t st = ws.stream;
+        const int tiles = std::max(1, (nn + kTileSize - 1) / kTileSize);
+        destTile.ensure((size_t)G * tiles);
+        KL(k_mask_tile_counts<<<tiles, kTileThreads, 0, st>>>(nn, destMask.p, G, tiles, destTile.p));
+        KL(k_mask_scan<<<G, 1024, 0, st>>>(tiles, destTile.p, destCountD.p));
+        std::vector<int> c(G);
+        CK(cudaMemcpyAsync(c.data(), destCountD.p, sizeof(int) * G, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        cnt.assign(G, 0);
+        start.assign(G, 0);
+        long long acc = 0;
+        std::vector<int> ds(G);
+        for (int q = 0; q < G; ++q) {
+            cnt[q] = c[q];
+            start[q] = acc;
+            ds[q] = (int)acc;
+            acc += c[q];
+        }
+        if (acc > n_capacity) fail(APBF_ERR_RUNTIME, "slab exchange exceeds the per-rank capacity");
+        CK(cudaMemcpyAsync(destStartD.p, ds.data(), sizeof(int) * G, cudaMemcpyHostToDevice, st));
+        KL(k_mask_scatter<<<tiles, kTileThreads, 0, st>>>(nn, destMask.p, G, tiles, destTile.p, destStartD.p,
+                                                        sendIdx.p));
+        LAUNCH_CHECK();
+    }
+
+    bool any_abort(Transport& T) {
+        T.allreduce(&ws.ctl.p->abort, 1, RType::I32, ROp::Max, ws.stream);
+        int a = 0;
+        CK(cudaMemcpy(&a, &ws.ctl.p->abort, sizeof(int), cudaMemcpyDeviceToHost));
+        return a != 0;
+    }
+
+    void run_lod_dist(Transport& T, const float4* X, int nn, long long nAll, const apbf_camera& cam,
+                      const apbf_lod_config& lod, int* LV) {
+        cudaStream_t st = ws.stream;
+        ws.dist.ensure(std::max(nn, 1));
+        ws.keys.ensure(std::max(nn, 1));
+        const bool dtvs = lod.model == APBF_LOD_DTVS;
+        if (dtvs) {
+            const CamFrame f = make_frame(cam);
+            const size_t px = (size_t)cam.width * cam.height;
+            ws.depth.ensure(px);
+            KL(k_fill_int<<<blocks((long long)px, 256), 256, 0, st>>>(ws.depth.p, (int)px, 0x7f800000));
+            KL(k_splat<<<blocks(nn, 256), 256, 0, st>>>(nn, X, radius, f, ws.depth.p));
+            T.allreduce(ws.depth.p, px, RType::I32, ROp::Min, st);  // positive float bits: int order
+            KL(k_dtvs_gap<<<blocks(nn, 256), 256, 0, st>>>(nn, X, radius, f, ws.depth.p, ws.dist.p,
+                                                         ws.keys.p, ws.ctl.p));
+            T.allreduce(&ws.ctl.p->sample_count, 1, RType::I32, ROp::Sum, st);
+        } else {
+            KL(k_dtc_dist<<<blocks(nn, 256), 256, 0, st>>>(nn, X, cam.eye[0], cam.eye[1], cam.eye[2],
+                                                         ws.dist.p, ws.keys.p));
+        }
+        if (lod.auto_range) {
+            KL(k_rs_init<<<1, 1, 0, st>>>(ws.rs.p, ws.ctl.p, (int)nAll, dtvs ? 1 : 0));
+            KL(k_rs_clear<<<1, 1024, 0, st>>>(ws.rs.p));
+            const int hb = std::min(blocks(nn, 256), 2 * 148);
+            for (int pass = 0; pass < 3; ++pass) {
+                KL(k_rs_hist<<<hb, 256, 0, st>>>(nn, ws.keys.p, ws.rs.p, pass));
+                T.allreduce(&ws.rs.p->hist[0][0], 4 * 2048, RType::U32, ROp::Sum, st);
+                KL(k_rs_select<<<1, 1024, 0, st>>>(ws.rs.p, pass));
+            }
+        }
+        KL(k_lod_params<<<1, 1, 0, st>>>(ws.rs.p, ws.ctl.p, lod.auto_range, lod.d_min, lod.d_max, dtvs ? 1 : 0));
+        KL(k_lod_map<<<blocks(nn, 256), 256, 0, st>>>(nn, ws.ctl.p, ws.dist.p, ws.keys.p, dtvs ? 1 : 0,
+                                                     lod.n_min, lod.n_max, LV));
+        LAUNCH_CHECK();
+    }
+
+    void run_frame_dist(Transport& T, std::vector<long long> cnt, bool assign_lod,
+                        const apbf_camera* cam, const apbf_lod_config* lod) {
+        const int G = T.size(), g = T.rank();
+        cudaStream_t st = ws.stream;
+        Ctl* ctl = ws.ctl.p;
+        const SolverConsts sc = consts();
+        const int nMax = cfg.n_max;
+        prefixPre.assign(cfg.substeps, 0);
+        prefixPost.assign(cfg.substeps, 0);
+        slab_error = false;
+        long long nAll = 0;
+        for (long long c : cnt) nAll += c;
+        CK(cudaEventRecord(ev[0], st));
+        KL(k_frame_begin<<<1, 1, 0, st>>>(ctl));
+        if (assign_lod) {
+            if (cfg.mode == APBF_MODE_PBF) {
+                KL(k_fill_int<<<blocks(n, 256), 256, 0, st>>>(set[cur].LV.p, n, nMax));
+            } else {
+                apbf_lod_config lc = *lod;
+                lc.n_min = cfg.n_min;
+                lc.n_max = cfg.n_max;
+                run_lod_dist(T, set[cur].X.p, n, nAll, *cam, lc, set[cur].LV.p);
+            }
+        }
+        for (int s = 0; s < cfg.substeps; ++s) {
+            prefixPre[s] = prefix_of(cnt, g);
+            StateSet src = set[cur].view(), dst = set[cur ^ 1].view();
+            KL(k_grid_reset<<<1, 1, 0, st>>>(ctl, 0));
+            KL(k_list_reset<<<1, 1, 0, st>>>(ctl));
+            KL(k_predict<<<blocks(n, 256), 256, 0, st>>>(n, src.X, src.V, src.XS, dt, cfg.gravity[0],
+                                                      cfg.gravity[1], cfg.gravity[2], ctl, s));
+            if (any_abort(T)) break;
+            // global grid: AABB all-reduce (ordered ints), identical params everywhere
+            T.allreduce(&ctl->grid[0].lo_ord[0], 3, RType::I32, ROp::Min, st);
+            T.allreduce(&ctl->grid[0].hi_ord[0], 3, RType::I32, ROp::Max, st);
+            KL(k_grid_params<<<1, 1, 0, st>>>(ctl, 0, cfg.h, cfg.h));
+            ws.read_ctl();
+            if (ws.h_ctl->runtime_error) break;
+            // slabs: equal-count split of the global per-layer histogram
+            const int dz = ws.h_ctl->grid[0].dims[2];
+            layerHist.ensure(dz);
+            CK(cudaMemsetAsync(layerHist.p, 0, sizeof(int) * dz, st));
+            KL(k_layer_hist<<<blocks(n, 256), 256, 0, st>>>(n, src.XS, ctl, 0, cfg.h, layerHist.p));
+            T.allreduce(layerHist.p, dz, RType::I32, ROp::Sum, st);
+            std::vector<int> h32(dz);
+            CK(cudaMemcpy(h32.data(), layerHist.p, sizeof(int) * dz, cudaMemcpyDeviceToHost));
+            std::vector<long long> hist(h32.begin(), h32.end());
+            std::vector<int> zr(2 * G);
+            if (!slab_partition(hist.data(), dz, G, 2, zr.data(), zr.data() + G)) {
+                slab_error = true;
+                break;
+            }
+            CK(cudaMemcpyAsync(zRange.p, zr.data(), sizeof(int) * 2 * G, cudaMemcpyHostToDevice, st));
+            // migration + halo in one all-to-all, previous global order kept
+            KL(k_dest_mask<<<blocks(n, 256), 256, 0, st>>>(n, src.XS, ctl, 0, cfg.h, zRange.p, zRange.p + G,
+                                                         G, 2, destMask.p));
+            std::vector<long long> sendCnt, sendStart, recvCnt(G);
+            expand_by_dest(n, G, sendCnt, sendStart);
+            const long long nsend = sendStart[G - 1] + sendCnt[G - 1];
+            KL(k_pack_recs<<<blocks(nsend, 256), 256, 0, st>>>((int)nsend, sendIdx.p, src, sendRec.p));
+            T.alltoall_counts(sendCnt.data(), recvCnt.data());
+            recvCnt[g] = sendCnt[g];
+            std::vector<long long> roff(G);
+            long long nLocal = 0;
+            for (int q = 0; q < G; ++q) {
+                roff[q] = nLocal;
+                nLocal += recvCnt[q];
+            }
+            if (nLocal > n_capacity) fail(APBF_ERR_RUNTIME, "slab holds more particles than the capacity");
+            std::vector<const void*> sp(G);
+            std::vector<void*> rp(G);
+            std::vector<size_t> sb(G), rb(G);
+            for (int q = 0; q < G; ++q) {
+                sp[q] = sendRec.p + sendStart[q];
+                sb[q] = sizeof(Rec) * sendCnt[q];
+                rp[q] = recvRec.p + roff[q];
+                rb[q] = sizeof(Rec) * recvCnt[q];
+            }
+            if (sendCnt[g])
+                CK(cudaMemcpyAsync(recvRec.p + roff[g], sendRec.p + sendStart[g], sizeof(Rec) * sendCnt[g],
+                                   cudaMemcpyDeviceToDevice, st));
+            T.alltoallv(sp.data(), sb.data(), rp.data(), rb.data(), st);
+            const int nL = (int)nLocal;
+            KL(k_unpack_recs<<<blocks(nL, 256), 256, 0, st>>>(nL, recvRec.p, src));
+            // local stable sort by global cell == global order restricted
+            ws.run_grid(0, src.XS, nL, cfg.h, cfg.h, false, radius);
+            const int tilesL = std::max(1, (nL + kTileSize - 1) / kTileSize);
+            const int smemG = (nMax + 1) * (int)sizeof(int);
+            KL(k_gather<<<tilesL, kTileThreads, smemG, st>>>(nL, ctl, ws.perm.p, src, dst, nMax, tilesL,
+                                                           tileCount.p));
+            KL(k_slab_bounds<<<1, 1, 0, st>>>(ctl, ws.cellCount.p, zr[g], zr[G + g], bounds.p));
+            int bd[6];
+            CK(cudaMemcpyAsync(bd, bounds.p, sizeof(bd), cudaMemcpyDeviceToHost, st));
+            CK(cudaStreamSynchronize(st));
+            const int ownB = bd[0], ownE = bd[1], l1B = bd[2], l1E = bd[3], lowEnd = bd[4], highB = bd[5];
+            const int nOwn = ownE - ownB;
+            if (scene.n > 0 && nOwn > 0)
+                KL(k_count_contacts<<<blocks(nOwn, 256), 256, 0, st>>>(nOwn, dst.XS + ownB, ws.scene.p, radius,
+                                                                     ctl));
+            if (nOwn > 0) KL(k_level_sum<<<blocks(nOwn, 256), 256, 0, st>>>(ownB, ownE, dst.LV, ctl));
+            // iteration order over owned + layer-1 ghosts (lambda is computed
+            // redundantly for the latter), outer ghosts never active
+            KL(k_mask_levels<<<blocks(nL, 256), 256, 0, st>>>(nL, dst.LV, l1B, l1E, LVo.p));
+            KL(k_level_tiles<<<tilesL, kTileThreads, smemG, st>>>(nL, ctl, LVo.p, nMax, tilesL, tileCount.p));
+            KL(k_level_scan<<<nMax + 1, 1024, 0, st>>>(ctl, tilesL, tileCount.p, levelCount.p));
+            KL(k_level_finish<<<1, 32, 0, st>>>(ctl, nL, nMax, levelCount.p, activeCount.p, bucketStart.p, 0));
+            KL(k_level_scatter<<<tilesL, kTileThreads, 9 * smemG, st>>>(nL, ctl, LVo.p, nMax, tilesL,
+                                                                       tileCount.p, bucketStart.p, order.p));
+            KL(k_build_lists<<<blocks(nL, 256), 256, 0, st>>>(nL, ctl, order.p, dst.XS, ws.cellCount.p, cfg.h,
+                                                           cfg.h * cfg.h, nbr.p, nbrCount.p, groupBase.p,
+                                                           nbrCap));
+            // pre-stabilization of every local copy with level < S (owners and
+            // ghost copies compute the same values); errors from owned only
+            if (S > 1)
+                KL(k_prestabilize_slots<<<blocks(nL, 256), 256, 0, st>>>(nL, ctl, S, dst.LV, dst.XS, dst.X,
+                                                                       ws.scene.p, radius, cfg.stab_iterations,
+                                                                       s, ownB, ownE));
+            LAUNCH_CHECK();
+            ownB_ = ownB;
+            ownE_ = ownE;
+            float4* P[2] = {dst.XS, PB.p};
+            for (int it = 1; it <= nMax; ++it) {
+                const float4* Pc = P[(it - 1) & 1];
+                float4* Pn = P[it & 1];
+                launch_solver_pair(it, s, Pc, Pn, dst, sc, -1);
+                if (cfg.record_residuals) {
+                    CK(cudaMemsetAsync(resid.p + (size_t)s * nMax + (it - 1), 0, sizeof(double), st));
+                    KL(k_residual<<<blocks(nL, 256), 256, 0, st>>>(nL, it, ctl, activeCount.p, order.p, Pn,
+                                                                nbr.p, nbrCount.p, groupBase.p, sc,
+                                                                resid.p + (size_t)s * nMax + (it - 1), ownB,
+                                                                ownE));
+                }
+                // halo: owned x* of the 2 boundary layers to each neighbour
+                std::vector<const void*> hs(G, nullptr);
+                std::vector<void*> hr(G, nullptr);
+                std::vector<size_t> hsb(G, 0), hrb(G, 0);
+                if (g > 0) {
+                    hs[g - 1] = Pn + ownB;
+                    hsb[g - 1] = sizeof(float4) * (size_t)(lowEnd - ownB);
+                    hr[g - 1] = Pn;
+                    hrb[g - 1] = sizeof(float4) * (size_t)ownB;
+                }
+                if (g < G - 1) {
+                    hs[g + 1] = Pn + highB;
+                    hsb[g + 1] = sizeof(float4) * (size_t)(ownE - highB);
+                    hr[g + 1] = Pn + ownE;
+                    hrb[g + 1] = sizeof(float4) * (size_t)(nL - ownE);
+                }
+                T.alltoallv(hs.data(), hsb.data(), hr.data(), hrb.data(), st);
+            }
+            ownB_ = 0;
+            ownE_ = 0x7fffffff;
+            float4* Pf = P[nMax & 1];
+            if (nOwn > 0)
+                KL(k_finalize<<<blocks(nOwn, 256), 256, 0, st>>>(nOwn, ctl, Pf + ownB, dst.XS + ownB, dst.X + ownB,
+                                                               dst.V + ownB, dt, cap, Pf != dst.XS ? 1 : 0, s));
+            LAUNCH_CHECK();
+            // keep only the owned particles, in order, as this rank's state
+            const size_t m = (size_t)nOwn;
+            if (m > 0) {
+                CK(cudaMemcpyAsync(src.X, dst.X + ownB, sizeof(float4) * m, cudaMemcpyDeviceToDevice, st));
+                CK(cudaMemcpyAsync(src.V, dst.V + ownB, sizeof(float4) * m, cudaMemcpyDeviceToDevice, st));
+                CK(cudaMemcpyAsync(src.XS, dst.XS + ownB, sizeof(float4) * m, cudaMemcpyDeviceToDevice, st));
+                CK(cudaMemcpyAsync(src.W, dst.W + ownB, sizeof(float) * m, cudaMemcpyDeviceToDevice, st));
+                CK(cudaMemcpyAsync(src.L, dst.L + ownB, sizeof(float) * m, cudaMemcpyDeviceToDevice, st));
+                CK(cudaMemcpyAsync(src.LV, dst.LV + ownB, sizeof(int) * m, cudaMemcpyDeviceToDevice, st));
+            }
+            n = nOwn;
+            cnt = all_counts(T, n);
+            prefixPost[s] = prefix_of(cnt, g);
+        }
+        CK(cudaEventRecord(ev[5], st));
+        const bool aborted = any_abort(T);
+        ws.read_ctl();
+        if (metrics && !aborted && !slab_error && !ws.h_ctl->runtime_error) run_metrics_dist(T);
+        T.allreduce(&ctl->total_iterations, 1, RType::I64, ROp::Sum, st);
+        T.allreduce(&ctl->contacts, 1, RType::I64, ROp::Sum, st);
+        T.allreduce(&ctl->list_overflow, 1, RType::I32, ROp::Max, st);
+        CK(cudaEventRecord(ev[6], st));
+        ws.read_ctl();
+    }
+
+    // allDensities(x) across slabs: owned particles plus every particle of
+    // other ranks within one metrics-grid layer of their layer range.
+    void run_metrics_dist(Transport& T) {
+        const int G = T.size(), g = T.rank();
+        cudaStream_t st = ws.stream;
+        Ctl* ctl = ws.ctl.p;
+        const StateSet cs = set[cur].view();
+        KL(k_grid_reset<<<1, 1, 0, st>>>(ctl, 1));
+        KL(k_aabb<<<blocks(n, 256), 256, 0, st>>>(n, cs.X, ctl, 1));
+        T.allreduce(&ctl->grid[1].lo_ord[0], 3, RType::I32, ROp::Min, st);
+        T.allreduce(&ctl->grid[1].hi_ord[0], 3, RType::I32, ROp::Max, st);
+        KL(k_grid_params<<<1, 1, 0, st>>>(ctl, 1, cfg.h, cfg.h));
+        int mm[2] = {0x7fffffff, (int)0x80000000};
+        CK(cudaMemcpyAsync(minmax.p, mm, sizeof(mm), cudaMemcpyHostToDevice, st));
+        KL(k_layer_minmax<<<blocks(n, 256), 256, 0, st>>>(n, cs.X, ctl, 1, cfg.h, minmax.p));
+        CK(cudaMemcpyAsync(mm, minmax.p, sizeof(mm), cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        std::vector<int> lo(G, 0x7fffffff), hi(G, (int)0x80000000);
+        lo[g] = mm[0];
+        hi[g] = mm[1];
+        CK(cudaMemcpyAsync(zRange.p, lo.data(), sizeof(int) * G, cudaMemcpyHostToDevice, st));
+        CK(cudaMemcpyAsync(zRange.p + G, hi.data(), sizeof(int) * G, cudaMemcpyHostToDevice, st));
+        T.allreduce(zRange.p, G, RType::I32, ROp::Min, st);
+        T.allreduce(zRange.p + G, G, RType::I32, ROp::Max, st);
+        CK(cudaMemcpy(lo.data(), zRange.p, sizeof(int) * G, cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(hi.data(), zRange.p + G, sizeof(int) * G, cudaMemcpyDeviceToHost));
+        for (int q = 0; q < G; ++q) {
+            if (q == g) {
+                lo[q] = -(1 << 29);
+                hi[q] = 1 << 29;
+            } else if (lo[q] > hi[q]) {
+                lo[q] = 1 << 29;  // empty rank
+                hi[q] = -(1 << 29);
+            } else {
+                hi[q] = hi[q] + 1;  // exclusive
+            }
+        }
+        CK(cudaMemcpyAsync(zRange.p, lo.data(), sizeof(int) * G, cudaMemcpyHostToDevice, st));
+        CK(cudaMemcpyAsync(zRange.p + G, hi.data(), sizeof(int) * G, cudaMemcpyHostToDevice, st));
+        KL(k_dest_mask<<<blocks(n, 256), 256, 0, st>>>(n, cs.X, ctl, 1, cfg.h, zRange.p, zRange.p + G, G, 1,
+                                                     destMask.p));
+        std::vector<long long> sendCnt, sendStart, recvCnt(G);
+        expand_by_dest(n, G, sendCnt, sendStart);
+        const long long nsend = sendStart[G - 1] + sendCnt[G - 1];
+        KL(k_pack_pm<<<blocks(nsend, 256), 256, 0, st>>>((int)nsend, sendIdx.p, cs.X, cs.XS, sendPM.p));
+        T.alltoall_counts(sendCnt.data(), recvCnt.data());
+        recvCnt[g] = sendCnt[g];
+        std::vector<long long> roff(G);
+        long long nM = 0;
+        for (int q = 0; q < G; ++q) {
+            roff[q] = nM;
+            nM += recvCnt[q];
+        }
+        std::vector<const void*> sp(G);
+        std::vector<void*> rp(G);
+        std::vector<size_t> sb(G), rb(G);
+        for (int q = 0; q < G; ++q) {
+            sp[q] = sendPM.p + sendStart[q];
+            sb[q] = sizeof(float4) * sendCnt[q];
+            rp[q] = recvPM.p + roff[q];
+            rb[q] = sizeof(float4) * recvCnt[q];
+        }
+        if (sendCnt[g])
+            CK(cudaMemcpyAsync(recvPM.p + roff[g], sendPM.p + sendStart[g], sizeof(float4) * sendCnt[g],
+                               cudaMemcpyDeviceToDevice, st));
+        T.alltoallv(sp.data(), sb.data(), rp.data(), rb.data(), st);
+        const int nm = (int)nM;
+        CK(cudaMemsetAsync(ownedFlag.p, 0, sizeof(int) * std::max(nm, 1), st));
+        if (sendCnt[g]) {
+            KL(k_fill_int<<<blocks(sendCnt[g], 256), 256, 0, st>>>(ownedFlag.p + roff[g], (int)sendCnt[g], 1));
+        }
+        ws.run_grid(1, recvPM.p, nm, cfg.h, cfg.h, false, radius);
+        KL(k_gather_posmass<<<blocks(nm, 256), 256, 0, st>>>(nm, ctl, ws.perm.p, recvPM.p, recvPM.p, sortedPM.p));
+        KL(k_gather_int<<<blocks(nm, 256), 256, 0, st>>>(nm, ws.perm.p, ownedFlag.p, ownedSorted.p));
+        KL(k_density_stats_owned<<<blocks(nm, 256), 256, 0, st>>>(nm, ctl, sortedPM.p, ownedSorted.p,
+                                                                ws.cellCount.p, make_kernel_consts(cfg.h)));
+        LAUNCH_CHECK();
+        T.allreduce(&ctl->rho_sum, 1, RType::F64, ROp::Sum, st);
+        T.allreduce(&ctl->rho_min_ord, 1, RType::I32, ROp::Min, st);
+        T.allreduce(&ctl->rho_max_ord, 1, RType::I32, ROp::Max, st);
+    }
+
+    void frame_dist(bool assign_lod, const apbf_camera* cam, const apbf_lod_config* lod, int frame_index,
+                    apbf_frame_stats* out) {
+        Transport& T = *transport;
+        const int G = T.size(), g = T.rank();
+        if (G > kMaxRanks) fail(APBF_ERR_INVALID_ARGUMENT, "too many slab ranks");
+        if (observer) fail(APBF_ERR_INVALID_ARGUMENT, "iteration observer is not available with slab decomposition");
+        std::vector<long long> cnt = all_counts(T, n);
+        long long nAll = 0;
+        for (long long c : cnt) nAll += c;
+        if (assign_lod && cfg.mode == APBF_MODE_APBF) {
+            apbf_lod_config lc = *lod;
+            validate_lod(lc);
+            if (nAll > 0 && lc.model == APBF_LOD_DTVS) {
+                if (!(radius > 0.0f)) fail(APBF_ERR_INVALID_ARGUMENT, "splat radius must be positive");
+                (void)make_frame(*cam);
+            }
+        }
+        apbf_frame_stats stt;
+        std::memset(&stt, 0, sizeof stt);
+        stt.frame = frame_index;
+        if (nAll > 0) {
+            const int start_set = cur;
+            const int start_n = n;
+            copy_set(backup, set[start_set]);
+            for (int attempt = 0;; ++attempt) {
+                run_frame_dist(T, cnt, assign_lod, cam, lod);
+                if (!ws.h_ctl->list_overflow) break;
+                if (attempt > 6) fail(APBF_ERR_RUNTIME, "neighbor list overflow");
+                cur = start_set;
+                n = start_n;
+                copy_set(set[cur], backup);
+                grow_lists(ws.h_ctl->list_alloc, ws.h_ctl->list_alloc_fb);
+            }
+            const Ctl& c = *ws.h_ctl;
+            if (c.runtime_error) fail(APBF_ERR_RUNTIME, "grid cell count exceeds limit; domain blew up");
+            if (slab_error) fail(APBF_ERR_RUNTIME, "too few grid layers for the slab decomposition");
+            // global first error: (substep, iteration, pass, global index)
+            const long long NONE = 0x7fffffffffffffffLL;
+            long long key = NONE;
+            int slotOf = -1;
+            for (int sl = 0; sl < kNumPassSlots; ++sl) {
+                if (c.bad[sl] == 0x7fffffff) continue;
+                const int sub = std::max(0, c.bad_substep[sl]);
+                const int itr = (sl == kPassLambda || sl == kPassApply) ? std::max(0, c.bad_iter[sl])
+                                : (sl >= kPassFinalizeV ? cfg.n_max + 1 : 0);
+                const long long gidx = (sl == kPassPredict ? prefixPre[sub] : prefixPost[sub]) + c.bad[sl];
+                const long long seq = ((long long)sub * (cfg.n_max + 2) + itr) * 8 + sl;
+                const long long k = (seq << 32) | gidx;
+                if (k < key) {
+                    key = k;
+                    slotOf = sl;
+                }
+            }
+            (void)slotOf;
+            long long* dkey = reinterpret_cast<long long*>(bounds.p);
+            CK(cudaMemcpy(dkey, &key, sizeof(key), cudaMemcpyHostToDevice));
+            T.allreduce(dkey, 1, RType::I64, ROp::Min, ws.stream);
+            CK(cudaMemcpy(&key, dkey, sizeof(key), cudaMemcpyDeviceToHost));
+            if (key != NONE) {
+                static const char* names[kNumPassSlots] = {"predict", "prestabilize", "lambda",
+                                                           "apply",   "finalize",     "finalize"};
+                static const char* details[kNumPassSlots] = {
+                    "non-finite predicted position", "non-finite predicted position", "non-finite lambda",
+                    "non-finite predicted position", "non-finite velocity",           "non-finite position"};
+                const int sl = (int)((key >> 32) & 7);
+                numerical(names[sl], (int)(key & 0xffffffffLL), details[sl]);
+            }
+            float ms = 0.f;
+            CK(cudaEventElapsedTime(&ms, ev[0], ev[5]));
+            stt.wall_ms = ms;
+            stt.total_iterations = (int64_t)c.total_iterations;
+            stt.contacts = (int64_t)c.contacts;
+            if (metrics) {
+                const double scale = 100.0 / (double)cfg.rest_density;
+                stt.avg_density_pct = c.rho_sum / (double)nAll * scale;
+                stt.min_density_pct = (double)ord2f(c.rho_min_ord) * scale;
+                stt.max_density_pct = (double)ord2f(c.rho_max_ord) * scale;
+            }
+            (void)g;
+        }
+        if (out) {
+            double* r = out->residuals;
+            int rc = out->residuals_capacity;
+            *out = stt;
             out->residuals = r;
             out->residuals_capacity = rc;
         }
@@ -1251,6 +1756,207 @@ int32_t apbf_gpu_count_contacts(int32_t n, const float* positions, const apbf_sd
         ws.read_ctl();
         *count_out = (int64_t)ws.h_ctl->contacts;
     });
+}
+
+
+// ------------------------------------------------- z-slab decomposition API
+
+struct apbf_gpu_group {
+    std::vector<std::unique_ptr<apbf_gpu_solver>> ranks;
+    std::unique_ptr<LoopbackHub> hub;
+    std::vector<std::unique_ptr<LoopbackTransport>> tr;
+    std::vector<int> devices;
+};
+
+static int32_t group_run(apbf_gpu_group* g, apbf_error* err,
+                         const std::function<void(apbf_gpu_solver&, int)>& fn) {
+    const int G = (int)g->ranks.size();
+    std::vector<apbf_error> errs(G);
+    std::vector<int32_t> rcs(G, APBF_OK);
+    g->hub->reset();
+    std::vector<std::thread> th;
+    for (int r = 0; r < G; ++r) {
+        th.emplace_back([&, r] {
+            rcs[r] = guarded(&errs[r], [&] {
+                CK(cudaSetDevice(g->devices[r]));
+                try {
+                    fn(*g->ranks[r], r);
+                } catch (...) {
+                    g->hub->poison();
+                    throw;
+                }
+            });
+        });
+    }
+    for (auto& t : th) t.join();
+    // a numerical / argument error is global (every rank reports the same);
+    // otherwise the first rank that failed for its own reason
+    for (int r = 0; r < G; ++r)
+        if (rcs[r] != APBF_OK && std::strcmp(errs[r].message, "slab peer rank failed") != 0) {
+            if (err) *err = errs[r];
+            return rcs[r];
+        }
+    for (int r = 0; r < G; ++r)
+        if (rcs[r] != APBF_OK) {
+            if (err) *err = errs[r];
+            return rcs[r];
+        }
+    return APBF_OK;
+}
+
+int32_t apbf_gpu_group_create(const apbf_solver_config* cfg, const apbf_sdf_primitive* prims,
+                              int32_t n_prims, float gradient_step, int32_t nranks,
+                              const int32_t* devices, apbf_gpu_group** out, apbf_error* err) {
+    return guarded(err, [&] {
+        *out = nullptr;
+        validate_config(cfg);
+        if (nranks < 1 || nranks > kMaxRanks) fail(APBF_ERR_INVALID_ARGUMENT, "slab rank count out of range");
+        const Scene sc = make_scene(prims, n_prims, gradient_step);
+        int count = 0;
+        CK(cudaGetDeviceCount(&count));
+        auto g = std::make_unique<apbf_gpu_group>();
+        for (int r = 0; r < nranks; ++r) {
+            const int d = devices ? devices[r] : 0;
+            if (d < 0 || d >= count) fail(APBF_ERR_INVALID_ARGUMENT, "CUDA device out of range");
+            g->devices.push_back(d);
+        }
+        for (int r = 0; r < nranks; ++r)
+            for (int q = 0; q < nranks; ++q)
+                if (g->devices[r] != g->devices[q]) {
+                    CK(cudaSetDevice(g->devices[r]));
+                    const cudaError_t e = cudaDeviceEnablePeerAccess(g->devices[q], 0);
+                    if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) CK(e);
+                    cudaGetLastError();
+                }
+        g->hub = std::make_unique<LoopbackHub>(nranks, g->devices);
+        for (int r = 0; r < nranks; ++r) {
+            CK(cudaSetDevice(g->devices[r]));
+            g->ranks.emplace_back(new apbf_gpu_solver(*cfg, sc, g->devices[r]));
+            g->tr.emplace_back(new LoopbackTransport(g->hub.get(), r));
+            g->ranks.back()->transport = g->tr.back().get();
+        }
+        *out = g.release();
+    });
+}
+
+void apbf_gpu_group_destroy(apbf_gpu_group* g) { delete g; }
+
+int32_t apbf_gpu_group_size(const apbf_gpu_group* g) { return g ? (int32_t)g->ranks.size() : 0; }
+
+int32_t apbf_gpu_group_set_state(apbf_gpu_group* g, int32_t n, const float* x, const float* xs,
+                                 const float* v, const float* mass, const float* inv_mass,
+                                 const float* lambda, const int32_t* level, apbf_error* err) {
+    if (n < 0) {
+        guarded(err, [] { fail(APBF_ERR_INVALID_ARGUMENT, "negative particle count"); });
+        return APBF_ERR_INVALID_ARGUMENT;
+    }
+    const int G = (int)g->ranks.size();
+    return group_run(g, err, [&](apbf_gpu_solver& s, int r) {
+        // rank r takes the contiguous storage range [n r / G, n (r+1) / G)
+        const long long b = (long long)n * r / G, e = (long long)n * (r + 1) / G;
+        s.set_state_local((int)(e - b), n, x + 3 * b, xs + 3 * b, v + 3 * b, mass + b, inv_mass + b,
+                          lambda + b, level + b);
+    });
+}
+
+int32_t apbf_gpu_group_particle_counts(const apbf_gpu_group* g, int32_t* counts) {
+    for (size_t r = 0; r < g->ranks.size(); ++r) counts[r] = g->ranks[r]->n;
+    return APBF_OK;
+}
+
+int32_t apbf_gpu_group_get_state(apbf_gpu_group* g, float* x, float* xs, float* v, float* mass,
+                                 float* inv_mass, float* lambda, int32_t* level, apbf_error* err) {
+    // global storage order = owned particles of rank 0, 1, ... (the slabs are
+    // increasing cell-layer ranges of the global cell order)
+    long long off = 0;
+    for (auto& s : g->ranks) {
+        const int32_t rc = apbf_gpu_get_state(s.get(), x ? x + 3 * off : nullptr, xs ? xs + 3 * off : nullptr,
+                                              v ? v + 3 * off : nullptr, mass ? mass + off : nullptr,
+                                              inv_mass ? inv_mass + off : nullptr, lambda ? lambda + off : nullptr,
+                                              level ? level + off : nullptr, err);
+        if (rc) return rc;
+        off += s->n;
+    }
+    return APBF_OK;
+}
+
+int32_t apbf_gpu_group_step_frame(apbf_gpu_group* g, const apbf_camera* cam, const apbf_lod_config* lod,
+                                  int32_t frame_index, apbf_frame_stats* out, apbf_error* err) {
+    const int G = (int)g->ranks.size();
+    std::vector<apbf_frame_stats> st(G);
+    std::vector<std::vector<double>> res(G);
+    for (int r = 0; r < G; ++r) {
+        std::memset(&st[r], 0, sizeof st[r]);
+        if (out && out->residuals) {
+            res[r].resize(out->residuals_capacity);
+            st[r].residuals = res[r].data();
+            st[r].residuals_capacity = out->residuals_capacity;
+        }
+    }
+    const int32_t rc = group_run(g, err, [&](apbf_gpu_solver& s, int r) {
+        s.frame(cam != nullptr, cam, lod, frame_index, &st[r]);
+        s.levels_valid = true;
+    });
+    if (rc == APBF_OK && out) {
+        double* rr = out->residuals;
+        const int cap = out->residuals_capacity;
+        *out = st[0];
+        out->residuals = rr;
+        out->residuals_capacity = cap;
+    }
+    return rc;
+}
+
+int32_t apbf_gpu_group_step_frame_with_levels(apbf_gpu_group* g, int32_t frame_index,
+                                              apbf_frame_stats* out, apbf_error* err) {
+    for (auto& s : g->ranks)
+        if (!s->levels_valid) {
+            guarded(err, [] { fail(APBF_ERR_INVALID_ARGUMENT, "particle level outside configured iteration range"); });
+            return APBF_ERR_INVALID_ARGUMENT;
+        }
+    return apbf_gpu_group_step_frame(g, nullptr, nullptr, frame_index, out, err);
+}
+
+int32_t apbf_gpu_nccl_unique_id(uint8_t* id128, apbf_error* err) {
+    return guarded(err, [&] {
+        NcclApi& api = NcclApi::get();
+        if (api.getUniqueId(id128) != 0) fail(APBF_ERR_CUDA, "ncclGetUniqueId failed");
+    });
+}
+
+int32_t apbf_gpu_solver_attach_nccl(apbf_gpu_solver* s, int32_t rank, int32_t nranks, const uint8_t* id128,
+                                    apbf_error* err) {
+    return guarded(err, [&] {
+        if (nranks < 1 || nranks > kMaxRanks || rank < 0 || rank >= nranks)
+            fail(APBF_ERR_INVALID_ARGUMENT, "slab rank out of range");
+        CK(cudaSetDevice(s->ws.device));
+        s->transport_owned.reset(new NcclTransport(rank, nranks, id128));
+        s->transport = s->transport_owned.get();
+    });
+}
+
+int32_t apbf_gpu_slab_set_state(apbf_gpu_solver* s, int32_t n_local, int64_t n_global, const float* x,
+                                const float* xs, const float* v, const float* mass, const float* inv_mass,
+                                const float* lambda, const int32_t* level, apbf_error* err) {
+    return guarded(err, [&] {
+        if (!s->transport) fail(APBF_ERR_INVALID_ARGUMENT, "solver is not attached to a slab transport");
+        CK(cudaSetDevice(s->ws.device));
+        s->set_state_local(n_local, n_global, x, xs, v, mass, inv_mass, lambda, level);
+    });
+}
+
+// Pure host logic of the decomposition, exposed for tests: equal-count
+// partition of a per-layer histogram into slabs of >= min_layers layers.
+int32_t apbf_slab_partition(const int64_t* layer_hist, int32_t layers, int32_t nranks, int32_t min_layers,
+                            int32_t* zlo, int32_t* zhi) {
+    std::vector<long long> h(layer_hist, layer_hist + layers);
+    std::vector<int> a(nranks), b(nranks);
+    if (!slab_partition(h.data(), layers, nranks, min_layers, a.data(), b.data())) return APBF_ERR_RUNTIME;
+    for (int g = 0; g < nranks; ++g) {
+        zlo[g] = a[g];
+        zhi[g] = b[g];
+    }
+    return APBF_OK;
 }
 
 }  // extern "C"

@@ -529,7 +529,7 @@ __global__ void __launch_bounds__(kTileP) k_residual_tile(
 __global__ void k_prestabilize_slots(int n, Ctl* ctl, int S, const int* __restrict__ LV,
                                      float4* __restrict__ XS, float4* __restrict__ X,
                                      const Scene* __restrict__ scene, float r, int iters,
-                                     int substep) {
+                                     int substep, int ownB = 0, int ownE = 0x7fffffff) {
     if (ctl->abort) return;
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     bool bad = false;
@@ -554,9 +554,9 @@ __global__ void k_prestabilize_slots(int n, Ctl* ctl, int S, const int* __restri
             XS[i] = s;
             X[i] = x;
         }
-        bad = !finite3(s.x, s.y, s.z);
+        bad = !finite3(s.x, s.y, s.z) && i >= ownB && i < ownE;
     }
-    report_bad(ctl, kPassPrestab, bad, i);
+    report_bad(ctl, kPassPrestab, bad, i - ownB);
     if (bad) ctl->bad_substep[kPassPrestab] = substep;
 }
 
