@@ -497,20 +497,21 @@ struct apbf_gpu_solver {
     bool use_stage = false, use_coef = true, use_tiles = false;
     int block_threads = 128;  // APBF_BLOCK: CTA size of the order-based passes
     int ownB_ = 0, ownE_ = 0x7fffffff;  // owned slot range (slab mode); everything otherwise
+    int n_iter = 0;                     // particles the solver passes cover (n, or owned+ghosts)
 
     template <bool kZ, bool kS, bool kC, int kBT>
     void launch_pair_bt(int it, int s, const float4* Pc, float4* Pn, const StateSet& dst,
                         const SolverConsts& sc, int tslot) {
         cudaStream_t st = ws.stream;
         Ctl* ctl = ws.ctl.p;
-        const int sb = blocks(n, kBT);
+        const int sb = blocks(n_iter, kBT);
         const int smem = kS ? kSolverSmem : 0;
-        KL(k_lambda<kS, kC, kBT><<<sb, kBT, smem, st>>>(n, it, ctl, activeCount.p, order.p, Pc, dst.W,
+        KL(k_lambda<kS, kC, kBT><<<sb, kBT, smem, st>>>(n_iter, it, ctl, activeCount.p, order.p, Pc, dst.W,
                                                          dst.L, nbr.p, nbrCount.p, groupBase.p, coef.p,
                                                          sc, s, ownB_, ownE_));
         if (tslot >= 0) CK(cudaEventRecord(kt_ev[tslot][1], st));
         KL(k_deltap_apply<kZ, kS, kC, kBT><<<sb, kBT, smem, st>>>(
-            n, it, ctl, activeCount.p, order.p, Pc, Pn, dst.W, dst.L, dst.LV, nbr.p, nbrCount.p,
+            n_iter, it, ctl, activeCount.p, order.p, Pc, Pn, dst.W, dst.L, dst.LV, nbr.p, nbrCount.p,
             groupBase.p, coef.p, ws.scene.p, sc, s, ownB_, ownE_));
     }
 
@@ -566,7 +567,7 @@ struct apbf_gpu_solver {
 
     void launch_solver_pair(int it, int s, const float4* Pc, float4* Pn, const StateSet& dst,
                             const SolverConsts& sc, int tslot) {
-        if (use_tiles) {
+        if (use_tiles && !transport) {
             const int v = (cfg.inactive_lambda_zero ? 2 : 0) | (use_coef ? 1 : 0);
             switch (v) {
                 case 0: launch_tile_pair_t<false, false>(it, s, Pc, Pn, dst, sc, tslot); break;
@@ -625,6 +626,7 @@ struct apbf_gpu_solver {
         const int nMax = cfg.n_max;
         CK(cudaEventRecord(ev[0], st));
         kt_used = 0;
+        n_iter = n;
         KL(k_frame_begin<<<1, 1, 0, st>>>(ctl));
         if (assign_lod) {
             if (cfg.mode == APBF_MODE_PBF) {
@@ -649,7 +651,7 @@ struct apbf_gpu_solver {
                                                            tileCount.p));
             KL(k_level_scan<<<nMax + 1, 1024, 0, st>>>(ctl, numTiles, tileCount.p, levelCount.p));
             KL(k_level_finish<<<1, 32, 0, st>>>(ctl, n, nMax, levelCount.p, activeCount.p, bucketStart.p));
-            if (use_tiles) {
+            if (use_tiles && !transport) {
                 KL(k_tile_build<<<numTilesP, kTileP, 0, st>>>(n, ctl, dst.XS, ws.cellCount.p, dst.LV, cfg.h,
                                                             cfg.h * cfg.h, tileInfo.p, tileRuns.p, tileMax.p,
                                                             lists16.p, listCap16, fbLists.p, fbCap,
@@ -881,8 +883,10 @@ struct apbf_gpu_solver {
     void set_state_local(int nloc, long long ntotal, const float* x, const float* xs, const float* v,
                          const float* mass, const float* inv_mass, const float* lambda,
                          const int32_t* level) {
-        allocate((int)std::max<long long>(ntotal, 1));
-        n_capacity = std::max<long long>(ntotal, 1);
+        // owned + ghost copies: a rank can hold more than n_global / G, and
+        // the sends of one rank (owned + ghost duplicates) more than n_global
+        n_capacity = 2 * std::max<long long>(ntotal, 1) + 4096;
+        allocate((int)n_capacity);
         destMask.ensure(n_capacity);
         sendIdx.ensure(n_capacity);
         LVo.ensure(n_capacity);
@@ -1026,6 +1030,13 @@ struct apbf_gpu_solver {
             T.allreduce(&ctl->grid[0].hi_ord[0], 3, RType::I32, ROp::Max, st);
             KL(k_grid_params<<<1, 1, 0, st>>>(ctl, 0, cfg.h, cfg.h));
             ws.read_ctl();
+            if (std::getenv("APBF_DEBUG_SLAB")) {
+                const GridDev& gd = ws.h_ctl->grid[0];
+                std::fprintf(stderr, "[slab %d/%d] s=%d n=%d lo=(%g %g %g) hi=(%g %g %g) dims=(%d %d %d) cells=%lld rt=%d\n",
+                             g, G, s, n, ord2f(gd.lo_ord[0]), ord2f(gd.lo_ord[1]), ord2f(gd.lo_ord[2]),
+                             ord2f(gd.hi_ord[0]), ord2f(gd.hi_ord[1]), ord2f(gd.hi_ord[2]), gd.dims[0], gd.dims[1],
+                             gd.dims[2], gd.cells, ws.h_ctl->runtime_error);
+            }
             if (ws.h_ctl->runtime_error) break;
             // slabs: equal-count split of the global per-layer histogram
             const int dz = ws.h_ctl->grid[0].dims[2];
@@ -1109,6 +1120,7 @@ struct apbf_gpu_solver {
             LAUNCH_CHECK();
             ownB_ = ownB;
             ownE_ = ownE;
+            n_iter = nL;
             float4* P[2] = {dst.XS, PB.p};
             for (int it = 1; it <= nMax; ++it) {
                 const float4* Pc = P[(it - 1) & 1];
