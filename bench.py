@@ -18,8 +18,10 @@ e2e    = the same metric through the reference-facing call with HOST buffers:
          cores) on the same workload.
 
 Usage: python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-N > 1 is launched by torchrun; every rank simulates its own 1M tank (weak
-scaling, independent tanks -- the z-slab decomposition is the next row).
+N > 1 is launched by torchrun (one process per GPU): the C3 ocean extended N
+times along z (1M particles per GPU, weak scaling) runs as ONE domain,
+z-slab decomposed with NCCL migration/halo exchanges (paper_1608_04721_b200/
+slab.py); every FrameStats total is global.
 """
 from __future__ import annotations
 
@@ -227,31 +229,43 @@ def run_reference(args, world, rank):
 
 
 def run_ours(args, world, rank, local, pg):
-    import ctypes as C
-
     import numpy as np
     import torch
 
     from paper_1608_04721_b200 import Solver
     from paper_1608_04721_b200 import scenario as S
+    from paper_1608_04721_b200.slab import SlabSolver, nccl_unique_id, slice_state
 
-    spec = S.build_scenario(args.scenario)
-    n = spec.particle_count()
-    solver = Solver(spec.solver, spec.scene, device=local)
-    state = S.make_state(spec, args.seed + rank)
-    solver.upload(state)
-    cam, lod = spec.camera, spec.lod
     torch.cuda.set_device(local)
+    if world == 1:
+        spec = S.build_scenario(args.scenario)
+    else:
+        spec = S.ocean_weak(world)
+    n_global = spec.particle_count()
+    cam, lod = spec.camera, spec.lod
+    if world == 1:
+        solver = Solver(spec.solver, spec.scene, device=local)
+        state = S.make_state(spec, args.seed)
+        solver.upload(state)
+    else:
+        # one process per GPU, NCCL communicator for the slab exchanges
+        uid = [nccl_unique_id() if rank == 0 else None]
+        pg.broadcast_object_list(uid, src=0)
+        solver = SlabSolver(spec.solver, spec.scene, rank, world, uid[0], device=local)
+        state = slice_state(S.make_state(spec, args.seed), rank, world)
+        solver.upload_slice(state, n_global)
     ext = torch.cuda.ExternalStream(solver.stream_handle(), device=local)
 
     for f in range(max(3, args.warmup)):
         solver.step_frame_resident(cam, lod, f)
 
     # ---------------- device-resident timed region ----------------
-    solver.set_kernel_timing(True)
+    if world == 1:
+        solver.set_kernel_timing(True)
     launches0 = Solver.launch_count()
     clocks = ClockSampler(local)
     clocks.start()
+    time.sleep(0.5)  # let nvidia-smi start sampling before the timed region
     barrier(pg)
     torch.cuda.synchronize()
     e0 = torch.cuda.Event(enable_timing=True)
@@ -259,7 +273,7 @@ def run_ours(args, world, rank, local, pg):
     e0.record(ext)
     its = 0
     for f in range(args.steps):
-        its += solver.step_frame_resident(cam, lod, 1000 + f).total_iterations
+        its += solver.step_frame_resident(cam, lod, 1000 + f).total_iterations  # global total
     e1.record(ext)
     e1.synchronize()
     torch.cuda.synchronize()
@@ -272,96 +286,126 @@ def run_ours(args, world, rank, local, pg):
     entries, _ = solver.last_neighbor_stats()
 
     ms_max = allreduce_max(pg, ms)
-    its_all = allreduce_sum(pg, float(its))
-    value = its_all / (ms_max / 1e3)
+    value = its / (ms_max / 1e3)  # FrameStats totals are already global
 
     # ---------------- e2e through the C-ABI with host buffers ----------------
     e2e = None
     if not args.no_e2e:
-        host = S.make_state(spec, args.seed + rank)
-        pinned = {}
-        for k in ("x", "x_star", "v", "mass", "inv_mass", "lambda_", "level"):
-            a = getattr(host, k)
-            t = torch.empty(a.shape, dtype=torch.from_numpy(a).dtype, pin_memory=True)
-            t.numpy()[...] = a
-            pinned[k] = t
-            setattr(host, k, t.numpy())
-        solver.upload(host)
+        host = S.make_state(spec, args.seed)
+        if world > 1:
+            host = slice_state(host, rank, world)
+        n_host = host.count()
+        cap = n_host if world == 1 else 2 * n_global // world + 4096
+
+        def pinned(shape, dtype):
+            return torch.empty(shape, dtype=dtype, pin_memory=True).numpy()
+
+        buf = {"x": pinned((cap, 3), torch.float32), "x_star": pinned((cap, 3), torch.float32),
+               "v": pinned((cap, 3), torch.float32), "mass": pinned(cap, torch.float32),
+               "inv_mass": pinned(cap, torch.float32), "lambda_": pinned(cap, torch.float32),
+               "level": pinned(cap, torch.int32)}
+        for k, a in buf.items():
+            a[:n_host] = getattr(host, k)
+
+        def view(m):
+            st = S.ParticleSet.__new__(S.ParticleSet)
+            for k, a in buf.items():
+                setattr(st, k, a[:m])
+            return st
+
+        def e2e_step(m, frame):
+            st = view(m)
+            if world == 1:
+                solver.upload(st)
+            else:
+                solver.upload_slice(st, n_global)
+            stats = solver.step_frame_resident(cam, lod, frame)
+            m2 = solver._lib.apbf_gpu_particle_count(solver._h)
+            out = view(m2)
+            solver.download(out)
+            return stats, m2
+
+        m = n_host
         for f in range(2):
-            solver.step_frame(host, cam, lod, f)
+            _, m = e2e_step(m, f)
         barrier(pg)
         torch.cuda.synchronize()
         e2 = torch.cuda.Event(enable_timing=True)
         e3 = torch.cuda.Event(enable_timing=True)
         e2.record(ext)
         its2 = 0
+        h2d = d2h = 0
         for f in range(args.steps):
-            its2 += solver.step_frame(host, cam, lod, 2000 + f).total_iterations
+            h2d += 52 * m
+            stats, m = e2e_step(m, 2000 + f)
+            d2h += 52 * m
+            its2 += stats.total_iterations
         e3.record(ext)
         e3.synchronize()
         barrier(pg)
         ms2 = allreduce_max(pg, e2.elapsed_time(e3))
-        its2_all = allreduce_sum(pg, float(its2))
-        words = 13  # x3 + x*3 + v3 + m + w + lambda + level
-        e2e = {"value": its2_all / (ms2 / 1e3), "unit": UNIT,
-               "h2d_bytes_per_step": 4 * words * n, "d2h_bytes_per_step": 4 * words * n,
+        h2d_all = allreduce_sum(pg, float(h2d)) / args.steps
+        d2h_all = allreduce_sum(pg, float(d2h)) / args.steps
+        e2e = {"value": its2 / (ms2 / 1e3), "unit": UNIT,
+               "h2d_bytes_per_step": int(h2d_all), "d2h_bytes_per_step": int(d2h_all),
                "ms_per_step": ms2 / args.steps,
-               "note": "per step: apbf_gpu_set_state from pinned host arrays + step_frame + "
-                       "apbf_gpu_get_state into them (the reference's stepFrame(ParticleSet&) contract)"}
+               "note": "per step: every rank uploads its particles from pinned host arrays "
+                       "(apbf_gpu_set_state / apbf_gpu_slab_set_state, 13 words each), steps, and "
+                       "downloads them (apbf_gpu_get_state) -- the reference's stepFrame(ParticleSet&) contract"}
 
     if rank != 0:
         return 0
 
     hbm_peak, peak_kind = peaks()
-    dom = "deltap_apply" if kt["deltap_ms"] >= kt["lambda_ms"] else "lambda"
-    dom_ms = kt["deltap_ms"] if dom == "deltap_apply" else kt["lambda_ms"]
-    per_launch_ms = dom_ms / max(1, kt["launches"])
-    pis_per_launch = kt["particle_iterations"] / max(1, kt["launches"])
-    alg_bytes = BYTES_PER_PI[dom] * pis_per_launch
-    achieved = alg_bytes / (per_launch_ms / 1e3) / 1e9
-    nbar = entries / n
-    # flops per particle-iteration from the reference expressions (SURVEY.md
-    # 8d): lambda 37 per non-self pair + 31, delta-p+apply 23 per pair + 4 (+3)
-    flops_pi = {"lambda": 37 * (nbar - 1) + 31, "deltap_apply": 23 * (nbar - 1) + 7}[dom]
-    sm_mhz = clk.get("sm_mhz") or 1965.0
-    fp32_peak = 148 * 128 * sm_mhz * 1e6 / 1e12  # non-FMA TFLOP/s (parity build, -fmad=false)
-    fp32_achieved = flops_pi * pis_per_launch / (per_launch_ms / 1e3) / 1e12
-
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": max(3, args.warmup), "ms_per_step": ms_max / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic",
-        "config": {"workload": f"{spec.name}: {n} particles/GPU, APBF "
+        "config": {"workload": f"{spec.name}: {n_global} particles ({n_global // world} per GPU), APBF "
                                f"{spec.solver.range.n_min}..{spec.solver.range.n_max}, "
                                f"lod={spec.lod.model.name.lower()}, {spec.solver.substeps} substeps, "
                                "metrics pass included",
-                   "scenario_file": f"scenarios/{args.scenario}.cfg", "seed": args.seed,
-                   "parallelism": f"{world} independent tanks (one per GPU)",
+                   "scenario_file": "scenarios/ocean_1m.cfg" + ("" if world == 1 else f" x{world} along z"),
+                   "seed": args.seed,
+                   "parallelism": "single GPU" if world == 1 else
+                   f"{world} z-slabs, NCCL migration+halo all-to-all per substep, x* halo per iteration",
                    "l2": "inputs larger than L2 (~0.5 GB device state + scratch per frame)"},
         "steps_per_s": args.steps / (ms_max / 1e3),
-        "particle_iterations_per_step": its_all / args.steps,
+        "particle_iterations_per_step": its / args.steps,
         "e2e": e2e,
         "gpu_launches": launches,
         "clocks": clk,
-        "roofline": {"bound": "hbm", "kernel": f"k_{dom}", "achieved": achieved,
-                     "peak": hbm_peak, "unit": "GB/s", "frac": achieved / hbm_peak,
-                     "peak_source": peak_kind, "traffic": ncu_traffic(f"k_{dom}"),
-                     "algorithmic_bytes_per_launch": alg_bytes,
-                     "avg_launch_ms": per_launch_ms, "launches": kt["launches"],
-                     "share_of_step": (kt["lambda_ms"] + kt["deltap_ms"]) / ms,
-                     "note": "FP32-issue-bound gather kernel; HBM fraction low by construction "
-                             "(SURVEY.md 8d), see roofline_fp32"},
-        "roofline_fp32": {"bound": "fp32", "achieved": fp32_achieved, "peak": fp32_peak,
-                          "unit": "TFLOP/s", "frac": fp32_achieved / fp32_peak,
-                          "nbar": nbar, "flops_per_particle_iteration": flops_pi,
-                          "peak_note": "148 SMs x 128 lanes x median SM clock, no FMA credit"},
-        "kernel_ms": {"lambda_total": kt["lambda_ms"], "deltap_apply_total": kt["deltap_ms"],
-                      "timed_region_total": ms},
     }
-    if world == 1 and not args.no_cpu_baseline:
-        res = cpu_reference_sample(S.build_scenario(args.scenario), args.seed, args.cpu_frames)
-        line["cpu_baseline"] = {k: res[k] for k in ("value", "unit", "cores", "kind", "sample")}
+    if world == 1:
+        dom = "deltap_apply" if kt["deltap_ms"] >= kt["lambda_ms"] else "lambda"
+        dom_ms = kt["deltap_ms"] if dom == "deltap_apply" else kt["lambda_ms"]
+        per_launch_ms = dom_ms / max(1, kt["launches"])
+        pis_per_launch = kt["particle_iterations"] / max(1, kt["launches"])
+        alg_bytes = BYTES_PER_PI[dom] * pis_per_launch
+        achieved = alg_bytes / (per_launch_ms / 1e3) / 1e9
+        nbar = entries / n_global
+        flops_pi = {"lambda": 37 * (nbar - 1) + 31, "deltap_apply": 23 * (nbar - 1) + 7}[dom]
+        sm_mhz = clk.get("sm_mhz") or 1965.0
+        fp32_peak = 148 * 128 * sm_mhz * 1e6 / 1e12
+        fp32_achieved = flops_pi * pis_per_launch / (per_launch_ms / 1e3) / 1e12
+        line["roofline"] = {"bound": "hbm", "kernel": f"k_{dom}", "achieved": achieved,
+                            "peak": hbm_peak, "unit": "GB/s", "frac": achieved / hbm_peak,
+                            "peak_source": peak_kind, "traffic": ncu_traffic(f"k_{dom}"),
+                            "algorithmic_bytes_per_launch": alg_bytes,
+                            "avg_launch_ms": per_launch_ms, "launches": kt["launches"],
+                            "share_of_step": (kt["lambda_ms"] + kt["deltap_ms"]) / ms,
+                            "note": "FP32-issue/latency-bound gather kernel; HBM fraction low by "
+                                    "construction (SURVEY.md 8d), see roofline_fp32"}
+        line["roofline_fp32"] = {"bound": "fp32", "achieved": fp32_achieved, "peak": fp32_peak,
+                                 "unit": "TFLOP/s", "frac": fp32_achieved / fp32_peak, "nbar": nbar,
+                                 "flops_per_particle_iteration": flops_pi,
+                                 "peak_note": "148 SMs x 128 lanes x median SM clock, no FMA credit"}
+        line["kernel_ms"] = {"lambda_total": kt["lambda_ms"], "deltap_apply_total": kt["deltap_ms"],
+                             "timed_region_total": ms}
+        if not args.no_cpu_baseline:
+            res = cpu_reference_sample(S.build_scenario(args.scenario), args.seed, args.cpu_frames)
+            line["cpu_baseline"] = {k: res[k] for k in ("value", "unit", "cores", "kind", "sample")}
     print(json.dumps(line), flush=True)
     return 0
 

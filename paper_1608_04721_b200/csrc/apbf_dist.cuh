@@ -22,12 +22,14 @@ __device__ __forceinline__ int layer_of(const GridDev& G, float h, float z) {
     return imin_std(imax_std(v, 0), G.dims[2] - 1);
 }
 
-// Particles per cz layer (global grid g) -> hist[dims.z].
-__global__ void k_layer_hist(int n, const float4* __restrict__ P, const Ctl* ctl, int g, float h,
-                             int* __restrict__ hist) {
+// Work per cz layer (global grid g) -> hist[dims.z]: each particle counts
+// with its level (its particle-iterations this substep), so equal-sum slabs
+// balance the solver work of APBF rather than the particle count.
+__global__ void k_layer_hist(int n, const float4* __restrict__ P, const int* __restrict__ LV,
+                             const Ctl* ctl, int g, float h, int* __restrict__ hist) {
     if (ctl->abort) return;
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < n) atomicAdd(&hist[layer_of(ctl->grid[g], h, P[i].z)], 1);
+    if (i < n) atomicAdd(&hist[layer_of(ctl->grid[g], h, P[i].z)], 1 + LV[i]);
 }
 
 // Destination bit mask: bit q set when cz in [lo[q] - halo, hi[q] + halo).

@@ -1038,11 +1038,11 @@ struct apbf_gpu_solver {
                              gd.dims[2], gd.cells, ws.h_ctl->runtime_error);
             }
             if (ws.h_ctl->runtime_error) break;
-            // slabs: equal-count split of the global per-layer histogram
+            // slabs: equal-work split (sum of 1 + level per layer) of the global histogram
             const int dz = ws.h_ctl->grid[0].dims[2];
             layerHist.ensure(dz);
             CK(cudaMemsetAsync(layerHist.p, 0, sizeof(int) * dz, st));
-            KL(k_layer_hist<<<blocks(n, 256), 256, 0, st>>>(n, src.XS, ctl, 0, cfg.h, layerHist.p));
+            KL(k_layer_hist<<<blocks(n, 256), 256, 0, st>>>(n, src.XS, src.LV, ctl, 0, cfg.h, layerHist.p));
             T.allreduce(layerHist.p, dz, RType::I32, ROp::Sum, st);
             std::vector<int> h32(dz);
             CK(cudaMemcpy(h32.data(), layerHist.p, sizeof(int) * dz, cudaMemcpyDeviceToHost));

@@ -415,3 +415,22 @@ def scenario_hash(spec: ScenarioSpec, seed: int) -> int:
     cap = sv.velocity_cap if sv.velocity_cap > 0 else sv.h / (sv.dt_frame / sv.substeps)
     s += _num(radius) + _num(cap) + _num(int(sv.inactive_lambda_zero))
     return fnv1a64(s.encode())
+
+
+def ocean_weak(nranks: int) -> ScenarioSpec:
+    """Weak-scaling tank for the slab decomposition: the C3 ocean layer
+    (scenarios/ocean_1m.cfg) repeated `nranks` times along z (the slab axis),
+    i.e. counts 200 x 50 x (100 * nranks) in a box nranks x deeper; 1M
+    particles per GPU and exactly ocean_1m at nranks = 1."""
+    spec = build_scenario("ocean_1m")
+    if nranks == 1:
+        return spec
+    b = spec.blocks[0]
+    b.counts = (b.counts[0], b.counts[1], b.counts[2] * nranks)
+    box = spec.scene.primitives[0]
+    c, he = list(box.center), list(box.half_extents)
+    c[2] *= nranks
+    he[2] *= nranks
+    spec.scene.primitives[0] = Box(tuple(c), tuple(he), box.interior)
+    spec.name = f"ocean_weak_{nranks}"
+    return spec

@@ -77,3 +77,26 @@ def test_slabs_report_numerical_error_like_single_gpu():
     with pytest.raises(NumericalError) as e2:
         SlabGroup(cfg, nranks=2, devices=[0, 0]).step_frame_with_levels(s.copy(), 0)
     assert (e1.value.pass_, e1.value.particle) == (e2.value.pass_, e2.value.particle) == ("predict", 23)
+
+
+def test_nccl_transport_single_rank_matches_plain_solver():
+    """The NCCL transport (dlopen'ed libnccl, ncclCommInitRank, all-reduce)
+    with a 1-rank communicator runs the slab frame and must equal Solver."""
+    from paper_1608_04721_b200.slab import SlabSolver, nccl_unique_id
+    spec = S.build_scenario("dam_break", 8000 / 216000)
+    spec.lod.model = LodModel.DTC
+    one = Solver(spec.solver, spec.scene)
+    nc = SlabSolver(spec.solver, spec.scene, 0, 1, nccl_unique_id())
+    a = S.make_state(spec, 1)
+    b = a.copy()
+    one.upload(a)
+    nc.upload_slice(b, b.count())
+    for f in range(3):
+        sa = one.step_frame_resident(spec.camera, spec.lod, f)
+        sb = nc.step_frame_resident(spec.camera, spec.lod, f)
+        assert (sa.total_iterations, sa.contacts, sa.min_density_pct) == \
+               (sb.total_iterations, sb.contacts, sb.min_density_pct)
+    one.download(a)
+    nc.download(b)
+    for k in FIELDS:
+        assert np.array_equal(getattr(a, k), getattr(b, k)), k
