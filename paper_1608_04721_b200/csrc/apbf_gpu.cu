@@ -414,7 +414,9 @@ struct apbf_gpu_solver {
         if (const char* v = std::getenv("APBF_COEF_CACHE")) use_coef = std::atoi(v) != 0;
         if (const char* v = std::getenv("APBF_TILES")) use_tiles = std::atoi(v) != 0;
         if (const char* v = std::getenv("APBF_BLOCK")) block_threads = std::atoi(v);
-        if (block_threads != 256 && block_threads != 512 && block_threads != 1024) block_threads = 128;
+        if (const char* v = std::getenv("APBF_CHUNK")) chunk = std::atoi(v);
+        if (chunk != 1 && chunk != 2 && chunk != 8) chunk = 4;
+        if (block_threads != 256) block_threads = 128;
         configure_carveouts();
         CK(cudaMemcpy(ws.scene.p, &scene, sizeof(Scene), cudaMemcpyHostToDevice));
         levelCount.ensure(cfg.n_max + 2);
@@ -496,32 +498,40 @@ struct apbf_gpu_solver {
     // lambda pass's cache.  Every variant is bit-identical.
     bool use_stage = false, use_coef = true, use_tiles = false;
     int block_threads = 128;  // APBF_BLOCK: CTA size of the order-based passes
+    int chunk = 4;            // APBF_CHUNK: neighbours gathered per batch (1, 2, 4, 8)
     int ownB_ = 0, ownE_ = 0x7fffffff;  // owned slot range (slab mode); everything otherwise
     int n_iter = 0;                     // particles the solver passes cover (n, or owned+ghosts)
 
-    template <bool kZ, bool kS, bool kC, int kBT>
-    void launch_pair_bt(int it, int s, const float4* Pc, float4* Pn, const StateSet& dst,
-                        const SolverConsts& sc, int tslot) {
+    template <bool kZ, bool kS, bool kC, int kBT, int kK>
+    void launch_pair_btk(int it, int s, const float4* Pc, float4* Pn, const StateSet& dst,
+                         const SolverConsts& sc, int tslot) {
         cudaStream_t st = ws.stream;
         Ctl* ctl = ws.ctl.p;
         const int sb = blocks(n_iter, kBT);
         const int smem = kS ? kSolverSmem : 0;
-        KL(k_lambda<kS, kC, kBT><<<sb, kBT, smem, st>>>(n_iter, it, ctl, activeCount.p, order.p, Pc, dst.W,
+        KL(k_lambda<kS, kC, kBT, kK><<<sb, kBT, smem, st>>>(n_iter, it, ctl, activeCount.p, order.p, Pc, dst.W,
                                                          dst.L, nbr.p, nbrCount.p, groupBase.p, coef.p,
                                                          sc, s, ownB_, ownE_));
         if (tslot >= 0) CK(cudaEventRecord(kt_ev[tslot][1], st));
-        KL(k_deltap_apply<kZ, kS, kC, kBT><<<sb, kBT, smem, st>>>(
+        KL(k_deltap_apply<kZ, kS, kC, kBT, kK><<<sb, kBT, smem, st>>>(
             n_iter, it, ctl, activeCount.p, order.p, Pc, Pn, dst.W, dst.L, dst.LV, nbr.p, nbrCount.p,
             groupBase.p, coef.p, ws.scene.p, sc, s, ownB_, ownE_));
+    }
+
+    template <bool kZ, bool kS, bool kC, int kBT>
+    void launch_pair_bt(int it, int s, const float4* Pc, float4* Pn, const StateSet& dst,
+                        const SolverConsts& sc, int tslot) {
+        if (kS || chunk == 1) launch_pair_btk<kZ, kS, kC, kBT, 1>(it, s, Pc, Pn, dst, sc, tslot);
+        else if (chunk == 2) launch_pair_btk<kZ, kS, kC, kBT, 2>(it, s, Pc, Pn, dst, sc, tslot);
+        else if (chunk == 4) launch_pair_btk<kZ, kS, kC, kBT, 4>(it, s, Pc, Pn, dst, sc, tslot);
+        else launch_pair_btk<kZ, kS, kC, kBT, 8>(it, s, Pc, Pn, dst, sc, tslot);
     }
 
     template <bool kZ, bool kS, bool kC>
     void launch_pair_t(int it, int s, const float4* Pc, float4* Pn, const StateSet& dst,
                        const SolverConsts& sc, int tslot) {
-        if (kS || block_threads == 128) launch_pair_bt<kZ, kS, kC, 128>(it, s, Pc, Pn, dst, sc, tslot);
-        else if (block_threads == 256) launch_pair_bt<kZ, kS, kC, 256>(it, s, Pc, Pn, dst, sc, tslot);
-        else if (block_threads == 512) launch_pair_bt<kZ, kS, kC, 512>(it, s, Pc, Pn, dst, sc, tslot);
-        else launch_pair_bt<kZ, kS, kC, 1024>(it, s, Pc, Pn, dst, sc, tslot);
+        if (kS || block_threads != 256) launch_pair_bt<kZ, kS, kC, 128>(it, s, Pc, Pn, dst, sc, tslot);
+        else launch_pair_bt<kZ, kS, kC, 256>(it, s, Pc, Pn, dst, sc, tslot);
     }
 
     // The gather passes want L1, not shared memory (they use none unless
@@ -543,8 +553,6 @@ struct apbf_gpu_solver {
     void configure_carveouts() {
         carveout_bt<128>();
         carveout_bt<256>();
-        carveout_bt<512>();
-        carveout_bt<1024>();
         cudaGetLastError();
     }
 
