@@ -383,6 +383,8 @@ struct apbf_gpu_solver {
     long long kt_launches = 0, kt_items = 0;
 
     void enable_kernel_timing(bool on) {
+        drop_graph();
+        eager_seen = false;
         kernel_timing = on;
         const size_t need = (size_t)cfg.substeps * cfg.n_max;
         while (on && kt_ev.size() < need) {
@@ -415,6 +417,7 @@ struct apbf_gpu_solver {
         if (const char* v = std::getenv("APBF_TILES")) use_tiles = std::atoi(v) != 0;
         if (const char* v = std::getenv("APBF_BLOCK")) block_threads = std::atoi(v);
         if (const char* v = std::getenv("APBF_CHUNK")) chunk = std::atoi(v);
+        if (const char* v = std::getenv("APBF_GRAPHS")) use_graphs = std::atoi(v) != 0;
         if (chunk != 1 && chunk != 2 && chunk != 8) chunk = 4;
         if (block_threads != 256) block_threads = 128;
         configure_carveouts();
@@ -425,10 +428,13 @@ struct apbf_gpu_solver {
         resid.ensure((size_t)cfg.substeps * cfg.n_max);
     }
     ~apbf_gpu_solver() {
+        drop_graph();
         for (auto& e : ev) cudaEventDestroy(e);
     }
 
     void allocate(int nn) {
+        drop_graph();
+        eager_seen = false;
         n = nn;
         const size_t m = (size_t)std::max(nn, 1);
         set[0].ensure(m);
@@ -512,7 +518,7 @@ struct apbf_gpu_solver {
         KL(k_lambda<kS, kC, kBT, kK><<<sb, kBT, smem, st>>>(n_iter, it, ctl, activeCount.p, order.p, Pc, dst.W,
                                                          dst.L, nbr.p, nbrCount.p, groupBase.p, coef.p,
                                                          sc, s, ownB_, ownE_));
-        if (tslot >= 0) CK(cudaEventRecord(kt_ev[tslot][1], st));
+        if (tslot >= 0) rec(kt_ev[tslot][1]);
         KL(k_deltap_apply<kZ, kS, kC, kBT, kK><<<sb, kBT, smem, st>>>(
             n_iter, it, ctl, activeCount.p, order.p, Pc, Pn, dst.W, dst.L, dst.LV, nbr.p, nbrCount.p,
             groupBase.p, coef.p, ws.scene.p, sc, s, ownB_, ownE_));
@@ -567,7 +573,7 @@ struct apbf_gpu_solver {
                                                                 tileMax.p, Pc, dst.W, dst.L, dst.LV,
                                                                 lists16.p, fbLists.p, nbrCount.p,
                                                                 coef16.p, sc, s));
-        if (tslot >= 0) CK(cudaEventRecord(kt_ev[tslot][1], st));
+        if (tslot >= 0) rec(kt_ev[tslot][1]);
         KL(k_deltap_tile<kZ, kC><<<numTilesP, kTileP, smemD, st>>>(
             n, it, ctl, tileInfo.p, tileRuns.p, tileMax.p, Pc, Pn, dst.W, dst.L, dst.LV, lists16.p,
             fbLists.p, nbrCount.p, coef16.p, ws.scene.p, sc, s));
@@ -622,17 +628,26 @@ struct apbf_gpu_solver {
         }
     }
 
+    // Event records that also work inside stream capture (graph event nodes).
+    bool capturing = false;
+    void rec(cudaEvent_t e) {
+        if (capturing) CK(cudaEventRecordWithFlags(e, ws.stream, cudaEventRecordExternal));
+        else CK(cudaEventRecord(e, ws.stream));
+    }
     void mark(int k) {
-        if (phase_timing) CK(cudaEventRecord(ev[k], ws.stream));
+        if (phase_timing) rec(ev[k]);
     }
 
     // One frame on the device; returns after the control block is on the host.
-    void run_frame(bool assign_lod, const apbf_camera* cam, const apbf_lod_config* lod) {
+    // Enqueue one frame on the solver stream (no host synchronisation unless an
+    // iteration observer is installed): captured as a CUDA Graph by frame().
+    void enqueue_frame(bool assign_lod, const apbf_camera* cam, const apbf_lod_config* lod) {
         cudaStream_t st = ws.stream;
         Ctl* ctl = ws.ctl.p;
         const SolverConsts sc = consts();
         const int nMax = cfg.n_max;
-        CK(cudaEventRecord(ev[0], st));
+        rec(ev[0]);
+        copy_set(backup, set[cur]);  // frame-start state for a list-overflow retry
         kt_used = 0;
         n_iter = n;
         KL(k_frame_begin<<<1, 1, 0, st>>>(ctl));
@@ -670,7 +685,7 @@ struct apbf_gpu_solver {
             } else {
                 KL(k_level_scatter<<<numTiles, kTileThreads, 9 * smemG, st>>>(
                     n, ctl, dst.LV, nMax, numTiles, tileCount.p, bucketStart.p, order.p));
-                KL(k_build_lists<<<blocks(n, 256), 256, 0, st>>>(n, ctl, order.p, dst.XS, ws.cellCount.p,
+                KL(k_build_lists<<<blocks(n, kListThreads), kListThreads, 0, st>>>(n, ctl, order.p, dst.XS, ws.cellCount.p,
                                                               cfg.h, cfg.h * cfg.h, nbr.p, nbrCount.p,
                                                               groupBase.p, nbrCap));
                 if (S > 1)
@@ -701,9 +716,9 @@ struct apbf_gpu_solver {
                 const float4* Pc = P[(it - 1) & 1];
                 float4* Pn = P[it & 1];
                 const int tslot = kernel_timing ? (int)kt_used++ : -1;
-                if (tslot >= 0) CK(cudaEventRecord(kt_ev[tslot][0], st));
+                if (tslot >= 0) rec(kt_ev[tslot][0]);
                 launch_solver_pair(it, s, Pc, Pn, dst, sc, tslot);
-                if (tslot >= 0) CK(cudaEventRecord(kt_ev[tslot][2], st));
+                if (tslot >= 0) rec(kt_ev[tslot][2]);
                 if (cfg.record_residuals) {
                     CK(cudaMemsetAsync(resid.p + (size_t)s * nMax + (it - 1), 0, sizeof(double), st));
                     if (use_tiles)
@@ -736,7 +751,7 @@ struct apbf_gpu_solver {
             cur ^= 1;
             mark(4);
         }
-        CK(cudaEventRecord(ev[5], st));
+        rec(ev[5]);
         if (metrics) {
             // allDensities(x) over a throwaway grid (solver.hpp:271-279).
             KL(k_grid_reset<<<1, 1, 0, st>>>(ctl, 1));
@@ -747,8 +762,94 @@ struct apbf_gpu_solver {
             KL(k_density_stats<<<blocks(n, 256), 256, 0, st>>>(n, ctl, sortedPM.p, ws.cellCount.p, sc.kc));
             LAUNCH_CHECK();
         }
-        CK(cudaEventRecord(ev[6], st));
-        ws.read_ctl();
+        rec(ev[6]);
+        CK(cudaMemcpyAsync(ws.h_ctl, ws.ctl.p, sizeof(Ctl), cudaMemcpyDeviceToHost, st));
+    }
+
+    void run_frame(bool assign_lod, const apbf_camera* cam, const apbf_lod_config* lod) {
+        enqueue_frame(assign_lod, cam, lod);
+        CK(cudaStreamSynchronize(ws.stream));
+    }
+
+    // ---- CUDA Graph of the whole frame (LOD + substeps + metrics) ----
+    struct GraphKey {
+        int start, assign_lod, metrics, ktime, ptime, n, flags;
+        long long caps[3];
+        apbf_camera cam;
+        apbf_lod_config lod;
+    };
+    bool use_graphs = true;  // APBF_GRAPHS=0 disables
+    bool graph_ok = false, eager_seen = false;
+    GraphKey gkey{}, seen_key{};
+    cudaGraphExec_t gexec = nullptr;
+    size_t kt_used_graph = 0;
+
+    GraphKey make_key(bool assign_lod, const apbf_camera* cam, const apbf_lod_config* lod) const {
+        GraphKey k;
+        std::memset(&k, 0, sizeof k);
+        k.start = cur;
+        k.assign_lod = assign_lod;
+        k.metrics = metrics;
+        k.ktime = kernel_timing;
+        k.ptime = phase_timing;
+        k.n = n;
+        k.flags = (use_tiles ? 1 : 0) | (use_stage ? 2 : 0) | (use_coef ? 4 : 0) | (chunk << 4) |
+                  (block_threads << 8);
+        k.caps[0] = nbrCap;
+        k.caps[1] = listCap16;
+        k.caps[2] = fbCap;
+        if (assign_lod && cam) k.cam = *cam;
+        if (assign_lod && lod) k.lod = *lod;
+        return k;
+    }
+    void drop_graph() {
+        if (gexec) cudaGraphExecDestroy(gexec);
+        gexec = nullptr;
+        graph_ok = false;
+    }
+
+    // One frame: replay the captured graph when nothing changed since the
+    // previous frame, capture it on the second frame with the same key, run
+    // eagerly otherwise (first frame, observer, configuration change).
+    void launch_frame(bool assign_lod, const apbf_camera* cam, const apbf_lod_config* lod) {
+        const GraphKey key = make_key(assign_lod, cam, lod);
+        const bool graphable = use_graphs && !observer;
+        cudaStream_t st = ws.stream;
+        if (graphable && graph_ok && std::memcmp(&key, &gkey, sizeof key) == 0) {
+            CK(cudaGraphLaunch(gexec, st));
+            cur = key.start ^ (cfg.substeps & 1);
+            kt_used = kt_used_graph;
+            CK(cudaStreamSynchronize(st));
+            return;
+        }
+        if (graphable && eager_seen && std::memcmp(&key, &seen_key, sizeof key) == 0) {
+            drop_graph();
+            cudaGraph_t g = nullptr;
+            CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+            capturing = true;
+            try {
+                enqueue_frame(assign_lod, cam, lod);
+                capturing = false;
+            } catch (...) {
+                capturing = false;
+                cudaStreamEndCapture(st, &g);
+                if (g) cudaGraphDestroy(g);
+                throw;
+            }
+            CK(cudaStreamEndCapture(st, &g));
+            CK(cudaGraphInstantiate(&gexec, g, 0));
+            cudaGraphDestroy(g);
+            kt_used_graph = kt_used;
+            gkey = key;
+            graph_ok = true;
+            CK(cudaGraphLaunch(gexec, st));
+            cur = key.start ^ (cfg.substeps & 1);
+            CK(cudaStreamSynchronize(st));
+            return;
+        }
+        run_frame(assign_lod, cam, lod);
+        seen_key = key;
+        eager_seen = true;
     }
 
     void frame(bool assign_lod, const apbf_camera* cam, const apbf_lod_config* lod, int frame_index,
@@ -780,9 +881,9 @@ struct apbf_gpu_solver {
             return;
         }
         const int start_set = cur;
-        copy_set(backup, set[start_set]);
         for (int attempt = 0;; ++attempt) {
-            run_frame(assign_lod, cam, lod);
+            if (attempt == 0) launch_frame(assign_lod, cam, lod);
+            else run_frame(assign_lod, cam, lod);
             if (!ws.h_ctl->list_overflow) break;
             // Neighbour storage too small: restore the frame-start state,
             // double the capacity and run the frame again.
@@ -790,6 +891,8 @@ struct apbf_gpu_solver {
             cur = start_set;
             copy_set(set[cur], backup);
             grow_lists(ws.h_ctl->list_alloc, ws.h_ctl->list_alloc_fb);
+            drop_graph();
+            eager_seen = false;
         }
         const Ctl& c = *ws.h_ctl;
         if (kernel_timing) collect_kernel_timing(c.total_iterations);
@@ -1116,7 +1219,7 @@ struct apbf_gpu_solver {
             KL(k_level_finish<<<1, 32, 0, st>>>(ctl, nL, nMax, levelCount.p, activeCount.p, bucketStart.p, 0));
             KL(k_level_scatter<<<tilesL, kTileThreads, 9 * smemG, st>>>(nL, ctl, LVo.p, nMax, tilesL,
                                                                        tileCount.p, bucketStart.p, order.p));
-            KL(k_build_lists<<<blocks(nL, 256), 256, 0, st>>>(nL, ctl, order.p, dst.XS, ws.cellCount.p, cfg.h,
+            KL(k_build_lists<<<blocks(nL, kListThreads), kListThreads, 0, st>>>(nL, ctl, order.p, dst.XS, ws.cellCount.p, cfg.h,
                                                            cfg.h * cfg.h, nbr.p, nbrCount.p, groupBase.p,
                                                            nbrCap));
             // pre-stabilization of every local copy with level < S (owners and
