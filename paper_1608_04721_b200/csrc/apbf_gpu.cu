@@ -345,6 +345,7 @@ struct apbf_gpu_solver {
     SetBufs backup;
     int cur = 0;
     DBuf<float4> PB;
+    DBuf<float4> PL;  // (x*, lambda) published by the lambda pass for the delta-p gathers
     DBuf<int> order, nbrCount, nbr, tileCount, levelCount, activeCount, bucketStart;
     DBuf<long long> groupBase;
     DBuf<float> coef;  // per-list-entry spiky coefficient, lambda -> delta-p
@@ -441,6 +442,7 @@ struct apbf_gpu_solver {
         set[1].ensure(m);
         backup.ensure(m);
         PB.ensure(m);
+        PL.ensure(m);
         order.ensure(m);
         const size_t groups = (m + 31) / 32 + 1;
         nbrCount.ensure(groups * 32);
@@ -515,13 +517,13 @@ struct apbf_gpu_solver {
         Ctl* ctl = ws.ctl.p;
         const int sb = blocks(n_iter, kBT);
         const int smem = kS ? kSolverSmem : 0;
-        KL(k_lambda<kS, kC, kBT, kK><<<sb, kBT, smem, st>>>(n_iter, it, ctl, activeCount.p, order.p, Pc, dst.W,
-                                                         dst.L, nbr.p, nbrCount.p, groupBase.p, coef.p,
-                                                         sc, s, ownB_, ownE_));
+        KL(k_lambda<kS, kC, kBT, kK, kZ><<<sb, kBT, smem, st>>>(n_iter, it, ctl, activeCount.p, order.p, Pc,
+                                                             dst.W, dst.L, nbr.p, nbrCount.p, groupBase.p,
+                                                             coef.p, sc, s, ownB_, ownE_, PL.p));
         if (tslot >= 0) rec(kt_ev[tslot][1]);
         KL(k_deltap_apply<kZ, kS, kC, kBT, kK><<<sb, kBT, smem, st>>>(
             n_iter, it, ctl, activeCount.p, order.p, Pc, Pn, dst.W, dst.L, dst.LV, nbr.p, nbrCount.p,
-            groupBase.p, coef.p, ws.scene.p, sc, s, ownB_, ownE_));
+            groupBase.p, coef.p, ws.scene.p, sc, s, ownB_, ownE_, PL.p));
     }
 
     template <bool kZ, bool kS, bool kC, int kBT>
