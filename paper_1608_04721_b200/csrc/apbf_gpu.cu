@@ -497,6 +497,10 @@ struct apbf_gpu_solver {
         sc.eps = cfg.epsilon;
         sc.radius = radius;
         sc.invRho0sq = sc.invRho0 * sc.invRho0;
+        // preconditions of k_lambda's cheap division-range test
+        volatile float sh = sc.kc.spiky * sc.kc.h;
+        volatile float shh = sh * sc.kc.h;
+        sc.fastDiv = (cfg.h > 0.0f && cfg.h <= 0x1p60f && sc.kc.spiky < 0.0f && -shh < 0x1p61f) ? 1 : 0;
         return sc;
     }
 
