@@ -10,7 +10,8 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libapbf_gpu.so")
+# APBF_LIB names an alternative in-tree build (A/B of compile-time variants)
+LIB_PATH = os.path.join(HERE, os.environ.get("APBF_LIB", "libapbf_gpu.so"))
 
 APBF_OK = 0
 APBF_ERR_INVALID_ARGUMENT = 1

@@ -13,6 +13,7 @@
 #include <array>
 
 #include "apbf_tiles.cuh"
+#include "apbf_c16.cuh"
 #include "apbf_dist.cuh"
 #include "apbf_transport.h"
 
@@ -348,7 +349,9 @@ struct apbf_gpu_solver {
     DBuf<float4> PL;  // (x*, lambda) published by the lambda pass for the delta-p gathers
     DBuf<int> order, nbrCount, nbr, tileCount, levelCount, activeCount, bucketStart;
     DBuf<long long> groupBase;
-    DBuf<float> coef;  // per-list-entry spiky coefficient, lambda -> delta-p
+    DBuf<float> coef;  // per-list-entry spiky coefficient, lambda -> delta-p (32-bit lists)
+    DBuf<unsigned short> nbr16;  // compact lists (APBF_C16, default)
+    DBuf<int4> lbase;            // compact lists: 3 layer bases + count per order position
     // cell-tile solver (apbf_tiles.cuh)
     DBuf<TileInfo> tileInfo;
     DBuf<int2> tileRuns;
@@ -416,6 +419,7 @@ struct apbf_gpu_solver {
         if (const char* v = std::getenv("APBF_STAGE_LISTS")) use_stage = std::atoi(v) != 0;
         if (const char* v = std::getenv("APBF_COEF_CACHE")) use_coef = std::atoi(v) != 0;
         if (const char* v = std::getenv("APBF_TILES")) use_tiles = std::atoi(v) != 0;
+        if (const char* v = std::getenv("APBF_C16")) use_c16 = std::atoi(v) != 0;
         if (const char* v = std::getenv("APBF_BLOCK")) block_threads = std::atoi(v);
         if (const char* v = std::getenv("APBF_CHUNK")) chunk = std::atoi(v);
         if (const char* v = std::getenv("APBF_GRAPHS")) use_graphs = std::atoi(v) != 0;
@@ -447,12 +451,10 @@ struct apbf_gpu_solver {
         const size_t groups = (m + 31) / 32 + 1;
         nbrCount.ensure(groups * 32);
         groupBase.ensure(groups);
+        lbase.ensure(groups * 32);
         if (nbrCap < (long long)m * 48 + 4096) {
             nbrCap = (long long)m * 48 + 4096;
-            nbr.release();
-            nbr.ensure((size_t)nbrCap);
-            coef.release();
-            coef.ensure((size_t)nbrCap);
+            alloc_lists();
         }
         numTiles = (int)((m + kTileSize - 1) / kTileSize);
         numTilesP = (int)((m + kTileP - 1) / kTileP);
@@ -509,6 +511,7 @@ struct apbf_gpu_solver {
     // delta-p pass recompute the spiky coefficients instead of reading the
     // lambda pass's cache.  Every variant is bit-identical.
     bool use_stage = false, use_coef = true, use_tiles = false;
+    bool use_c16 = false;  // APBF_C16=1: compact 16-bit lists (slower here: the passes are latency-bound)
     int block_threads = 128;  // APBF_BLOCK: CTA size of the order-based passes
     int chunk = 4;            // APBF_CHUNK: neighbours gathered per batch (1, 2, 4, 8)
     int ownB_ = 0, ownE_ = 0x7fffffff;  // owned slot range (slab mode); everything otherwise
@@ -528,6 +531,52 @@ struct apbf_gpu_solver {
         KL(k_deltap_apply<kZ, kS, kC, kBT, kK><<<sb, kBT, smem, st>>>(
             n_iter, it, ctl, activeCount.p, order.p, Pc, Pn, dst.W, dst.L, dst.LV, nbr.p, nbrCount.p,
             groupBase.p, coef.p, ws.scene.p, sc, s, ownB_, ownE_, PL.p));
+    }
+
+    template <bool kZ, int kBT, int kK, bool kC>
+    void launch_pair_c16(int it, int s, const float4* Pc, float4* Pn, const StateSet& dst,
+                         const SolverConsts& sc, int tslot) {
+        cudaStream_t st = ws.stream;
+        Ctl* ctl = ws.ctl.p;
+        const int sb = blocks(n_iter, kBT);
+        KL(k_lambda_c16<kBT, kK, kZ, kC><<<sb, kBT, 0, st>>>(n_iter, it, ctl, activeCount.p, order.p, Pc, dst.W,
+                                                             dst.L, nbr16.p, lbase.p, groupBase.p, sc, s, ownB_,
+                                                             ownE_, PL.p, coef.p));
+        if (tslot >= 0) rec(kt_ev[tslot][1]);
+        KL(k_deltap_c16<kBT, kK, kC><<<sb, kBT, 0, st>>>(n_iter, it, ctl, activeCount.p, order.p, Pc, Pn, dst.W,
+                                                         dst.L, nbr16.p, lbase.p, groupBase.p, ws.scene.p, sc, s,
+                                                         ownB_, ownE_, PL.p, coef.p));
+    }
+    template <bool kZ, bool kC>
+    void launch_pair_c16_t(int it, int s, const float4* Pc, float4* Pn, const StateSet& dst,
+                           const SolverConsts& sc, int tslot) {
+        if (block_threads == 256) launch_pair_c16<kZ, 256, 4, kC>(it, s, Pc, Pn, dst, sc, tslot);
+        else launch_pair_c16<kZ, 128, 4, kC>(it, s, Pc, Pn, dst, sc, tslot);
+    }
+
+    // The list build and the residual pass for the current list encoding.
+    void launch_build_lists(int nn, const StateSet& dst) {
+        cudaStream_t st = ws.stream;
+        if (use_c16)
+            KL(k_build_lists<true><<<blocks(nn, kListThreads), kListThreads, 0, st>>>(
+                nn, ws.ctl.p, order.p, dst.XS, ws.cellCount.p, cfg.h, cfg.h * cfg.h, nbr.p, nbrCount.p,
+                groupBase.p, nbrCap, nbr16.p, lbase.p));
+        else
+            KL(k_build_lists<false><<<blocks(nn, kListThreads), kListThreads, 0, st>>>(
+                nn, ws.ctl.p, order.p, dst.XS, ws.cellCount.p, cfg.h, cfg.h * cfg.h, nbr.p, nbrCount.p,
+                groupBase.p, nbrCap, nbr16.p, lbase.p));
+    }
+    void launch_residual(int nn, int it, const float4* Pn, const SolverConsts& sc, double* out, int oB,
+                         int oE) {
+        cudaStream_t st = ws.stream;
+        if (use_c16)
+            KL(k_residual<true><<<blocks(nn, 256), 256, 0, st>>>(nn, it, ws.ctl.p, activeCount.p, order.p, Pn,
+                                                                 nbr.p, nbrCount.p, groupBase.p, sc, out, oB,
+                                                                 oE, nbr16.p, lbase.p));
+        else
+            KL(k_residual<false><<<blocks(nn, 256), 256, 0, st>>>(nn, it, ws.ctl.p, activeCount.p, order.p,
+                                                                  Pn, nbr.p, nbrCount.p, groupBase.p, sc, out,
+                                                                  oB, oE, nbr16.p, lbase.p));
     }
 
     template <bool kZ, bool kS, bool kC, int kBT>
@@ -597,6 +646,16 @@ struct apbf_gpu_solver {
             }
             return;
         }
+        if (use_c16) {
+            const int v = (cfg.inactive_lambda_zero ? 2 : 0) | (use_coef ? 1 : 0);
+            switch (v) {
+                case 0: launch_pair_c16_t<false, false>(it, s, Pc, Pn, dst, sc, tslot); break;
+                case 1: launch_pair_c16_t<false, true>(it, s, Pc, Pn, dst, sc, tslot); break;
+                case 2: launch_pair_c16_t<true, false>(it, s, Pc, Pn, dst, sc, tslot); break;
+                default: launch_pair_c16_t<true, true>(it, s, Pc, Pn, dst, sc, tslot); break;
+            }
+            return;
+        }
         const int v = (cfg.inactive_lambda_zero ? 4 : 0) | (use_stage ? 2 : 0) | (use_coef ? 1 : 0);
         switch (v) {
             case 0: launch_pair_t<false, false, false>(it, s, Pc, Pn, dst, sc, tslot); break;
@@ -610,14 +669,25 @@ struct apbf_gpu_solver {
         }
     }
 
-    // After an overflowed list build: grow whichever store ran out.
+    // (Re)allocate the order-based list store at nbrCap entries: compact
+    // 16-bit entries, or 32-bit entries plus the coefficient cache.
+    void alloc_lists() {
+        nbr.release();
+        coef.release();
+        nbr16.release();
+        if (use_c16) nbr16.ensure((size_t)nbrCap);
+        else nbr.ensure((size_t)nbrCap);
+        if (use_coef || !use_c16) coef.ensure((size_t)nbrCap);
+    }
+
+    // After an overflowed list build: leave the compact encoding when its
+    // offsets ran out of range (bit 2), grow whichever store ran out (bit 1).
     void grow_lists(unsigned long long used, unsigned long long used_fb) {
+        const int why = ws.h_ctl->list_overflow;
         if (!use_tiles) {
-            nbrCap = std::max<long long>(nbrCap * 2, (long long)(used * 3 / 2));
-            nbr.release();
-            nbr.ensure((size_t)nbrCap);
-            coef.release();
-            coef.ensure((size_t)nbrCap);
+            if (why & 2) use_c16 = false;
+            if (why & 1) nbrCap = std::max<long long>(nbrCap * 2, (long long)(used * 3 / 2));
+            alloc_lists();
             return;
         }
         if (used > (unsigned long long)listCap16) {
@@ -691,9 +761,7 @@ struct apbf_gpu_solver {
             } else {
                 KL(k_level_scatter<<<numTiles, kTileThreads, 9 * smemG, st>>>(
                     n, ctl, dst.LV, nMax, numTiles, tileCount.p, bucketStart.p, order.p));
-                KL(k_build_lists<<<blocks(n, kListThreads), kListThreads, 0, st>>>(n, ctl, order.p, dst.XS, ws.cellCount.p,
-                                                              cfg.h, cfg.h * cfg.h, nbr.p, nbrCount.p,
-                                                              groupBase.p, nbrCap));
+                launch_build_lists(n, dst);
                 if (S > 1)
                     KL(k_prestabilize<<<blocks(n, 256), 256, 0, st>>>(n, ctl, activeCount.p, S, order.p,
                                                                    dst.XS, dst.X, ws.scene.p, radius,
@@ -732,9 +800,7 @@ struct apbf_gpu_solver {
                             n, it, ctl, activeCount.p, tileInfo.p, tileRuns.p, Pn, lists16.p, fbLists.p,
                             nbrCount.p, sc, resid.p + (size_t)s * nMax + (it - 1)));
                     else
-                        KL(k_residual<<<blocks(n, 256), 256, 0, st>>>(n, it, ctl, activeCount.p, order.p, Pn,
-                                                                   nbr.p, nbrCount.p, groupBase.p, sc,
-                                                                   resid.p + (size_t)s * nMax + (it - 1)));
+                        launch_residual(n, it, Pn, sc, resid.p + (size_t)s * nMax + (it - 1), 0, 0x7fffffff);
                 }
                 LAUNCH_CHECK();
                 if (observer) {
@@ -799,7 +865,7 @@ struct apbf_gpu_solver {
         k.ktime = kernel_timing;
         k.ptime = phase_timing;
         k.n = n;
-        k.flags = (use_tiles ? 1 : 0) | (use_stage ? 2 : 0) | (use_coef ? 4 : 0) | (chunk << 4) |
+        k.flags = (use_tiles ? 1 : 0) | (use_stage ? 2 : 0) | (use_coef ? 4 : 0) | (use_c16 ? 8 : 0) | (chunk << 4) |
                   (block_threads << 8);
         k.caps[0] = nbrCap;
         k.caps[1] = listCap16;
@@ -914,6 +980,7 @@ struct apbf_gpu_solver {
         // (finalize: velocity before position) can hold a record.
         for (int s = 0; s < kNumPassSlots; ++s)
             if (c.bad[s] != 0x7fffffff) numerical(names[s], c.bad[s], details[s]);
+        if (c.abort) fail(APBF_ERR_RUNTIME, "frame aborted without a recorded cause");
         float ms = 0.f;
         CK(cudaEventElapsedTime(&ms, ev[0], ev[5]));
         st.wall_ms = ms;
@@ -1225,9 +1292,7 @@ struct apbf_gpu_solver {
             KL(k_level_finish<<<1, 32, 0, st>>>(ctl, nL, nMax, levelCount.p, activeCount.p, bucketStart.p, 0));
             KL(k_level_scatter<<<tilesL, kTileThreads, 9 * smemG, st>>>(nL, ctl, LVo.p, nMax, tilesL,
                                                                        tileCount.p, bucketStart.p, order.p));
-            KL(k_build_lists<<<blocks(nL, kListThreads), kListThreads, 0, st>>>(nL, ctl, order.p, dst.XS, ws.cellCount.p, cfg.h,
-                                                           cfg.h * cfg.h, nbr.p, nbrCount.p, groupBase.p,
-                                                           nbrCap));
+            launch_build_lists(nL, dst);
             // pre-stabilization of every local copy with level < S (owners and
             // ghost copies compute the same values); errors from owned only
             if (S > 1)
@@ -1245,10 +1310,7 @@ struct apbf_gpu_solver {
                 launch_solver_pair(it, s, Pc, Pn, dst, sc, -1);
                 if (cfg.record_residuals) {
                     CK(cudaMemsetAsync(resid.p + (size_t)s * nMax + (it - 1), 0, sizeof(double), st));
-                    KL(k_residual<<<blocks(nL, 256), 256, 0, st>>>(nL, it, ctl, activeCount.p, order.p, Pn,
-                                                                nbr.p, nbrCount.p, groupBase.p, sc,
-                                                                resid.p + (size_t)s * nMax + (it - 1), ownB,
-                                                                ownE));
+                    launch_residual(nL, it, Pn, sc, resid.p + (size_t)s * nMax + (it - 1), ownB, ownE);
                 }
                 // halo: owned x* of the 2 boundary layers to each neighbour
                 std::vector<const void*> hs(G, nullptr);
@@ -1421,7 +1483,6 @@ struct apbf_gpu_solver {
             // global first error: (substep, iteration, pass, global index)
             const long long NONE = 0x7fffffffffffffffLL;
             long long key = NONE;
-            int slotOf = -1;
             for (int sl = 0; sl < kNumPassSlots; ++sl) {
                 if (c.bad[sl] == 0x7fffffff) continue;
                 const int sub = std::max(0, c.bad_substep[sl]);
@@ -1430,12 +1491,8 @@ struct apbf_gpu_solver {
                 const long long gidx = (sl == kPassPredict ? prefixPre[sub] : prefixPost[sub]) + c.bad[sl];
                 const long long seq = ((long long)sub * (cfg.n_max + 2) + itr) * 8 + sl;
                 const long long k = (seq << 32) | gidx;
-                if (k < key) {
-                    key = k;
-                    slotOf = sl;
-                }
+                key = std::min(key, k);
             }
-            (void)slotOf;
             long long* dkey = reinterpret_cast<long long*>(bounds.p);
             CK(cudaMemcpy(dkey, &key, sizeof(key), cudaMemcpyHostToDevice));
             T.allreduce(dkey, 1, RType::I64, ROp::Min, ws.stream);
@@ -1449,6 +1506,7 @@ struct apbf_gpu_solver {
                 const int sl = (int)((key >> 32) & 7);
                 numerical(names[sl], (int)(key & 0xffffffffLL), details[sl]);
             }
+            if (c.abort) fail(APBF_ERR_RUNTIME, "frame aborted without a recorded cause");
             float ms = 0.f;
             CK(cudaEventElapsedTime(&ms, ev[0], ev[5]));
             stt.wall_ms = ms;

@@ -226,7 +226,7 @@ __global__ void __launch_bounds__(kTileP) k_tile_build(
             over = base + need > (unsigned long long)listCap;
         }
         if (over) {
-            ctl->list_overflow = 1;
+            atomicOr(&ctl->list_overflow, 1);
             ctl->abort = 1;
         }
         s_base = (unsigned)base;

@@ -1,0 +1,77 @@
+"""Every solver-pass variant selectable by environment (A/B switches read at
+Solver creation) must give the default path's frames bit for bit: compact
+16-bit lists with and without the coefficient cache, shared-memory list
+staging, the cell-tile solver, gather batch sizes, CTA size, eager launches
+instead of CUDA Graph replay.  Also the compact lists' range fallback."""
+import numpy as np
+import pytest
+
+from paper_1608_04721_b200 import IterationRange, LodModel, ParticleSet, Solver
+from paper_1608_04721_b200 import scenario as S
+
+pytestmark = pytest.mark.gpu
+
+FIELDS = ("x", "x_star", "v", "mass", "inv_mass", "lambda_", "level")
+VARIANTS = [
+    {"APBF_C16": "1"},
+    {"APBF_C16": "1", "APBF_COEF_CACHE": "0"},
+    {"APBF_COEF_CACHE": "0"},
+    {"APBF_STAGE_LISTS": "1"},
+    {"APBF_TILES": "1"},
+    {"APBF_CHUNK": "1"},
+    {"APBF_CHUNK": "2"},
+    {"APBF_CHUNK": "8"},
+    {"APBF_BLOCK": "256"},
+    {"APBF_GRAPHS": "0"},
+]
+
+
+def frames(spec, n, seed=1):
+    sv = Solver(spec.solver, spec.scene)
+    st = S.make_state(spec, seed)
+    stats = [sv.step_frame(st, spec.camera, spec.lod, f) for f in range(n)]
+    return st, [(s.total_iterations, s.contacts, s.min_density_pct, s.max_density_pct) for s in stats]
+
+
+def spec_apbf(zero_lambda):
+    spec = S.build_scenario("dam_break", 15625 / 216000)
+    spec.solver.range = IterationRange(5, 10)
+    spec.solver.inactive_lambda_zero = zero_lambda
+    spec.lod.range = spec.solver.range
+    spec.lod.model = LodModel.DTVS
+    return spec
+
+
+@pytest.mark.parametrize("zero_lambda", [False, True])
+@pytest.mark.parametrize("env", VARIANTS, ids=lambda e: ",".join(f"{k}={v}" for k, v in e.items()))
+def test_variant_matches_default(monkeypatch, env, zero_lambda):
+    spec = spec_apbf(zero_lambda)
+    ref, ref_stats = frames(spec, 5)
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    got, got_stats = frames(spec, 5)
+    assert got_stats == ref_stats
+    for k in FIELDS:
+        assert np.array_equal(getattr(ref, k), getattr(got, k)), k
+
+
+def test_compact_lists_fall_back_when_offsets_overflow(monkeypatch):
+    """A 3000-cell-long sheet puts > 2^14 slots between a particle's first
+    and last candidate rows of one layer: the compact build flags it and the
+    frame is re-run on 32-bit lists, with the same result as starting there."""
+    h = 0.1
+    nx, ny = 6000, 6  # 2 particles per cell along x and y
+    xs, ys = np.meshgrid(np.arange(nx) * (h / 2), np.arange(ny) * (h / 2), indexing="ij")
+    x = np.stack([xs.ravel(), ys.ravel(), np.full(xs.size, 0.5)], 1).astype(np.float32)
+    cfg = S.build_scenario("dam_break", 0.01).solver
+    cfg.h = h
+    cfg.range = IterationRange(2, 3)
+    cfg.gravity = (0.0, 0.0, 0.0)
+    base = ParticleSet(x, 0.01, 3)
+    a = base.copy()
+    Solver(cfg).step_frame_with_levels(a, 0)
+    monkeypatch.setenv("APBF_C16", "1")
+    b = base.copy()
+    Solver(cfg).step_frame_with_levels(b, 0)
+    for k in FIELDS:
+        assert np.array_equal(getattr(a, k), getattr(b, k)), k

@@ -5,7 +5,8 @@ from paper_1608_04721_b200 import Solver
 from paper_1608_04721_b200 import scenario as S
 name = sys.argv[1] if len(sys.argv) > 1 else "ocean_1m"
 frames = int(sys.argv[2]) if len(sys.argv) > 2 else 12
-spec = S.build_scenario(name)
+scale = float(sys.argv[3]) if len(sys.argv) > 3 else 1.0
+spec = S.build_scenario(name, scale)
 sv = Solver(spec.solver, spec.scene)
 st = S.make_state(spec, 1)
 sv.upload(st)
