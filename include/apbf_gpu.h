@@ -146,7 +146,9 @@ void apbf_gpu_solver_destroy(apbf_gpu_solver* s);
 
 /* Upload / download the ParticleSet (particle_state.hpp:33-42) in storage
  * order.  3-vector arrays hold 3*n floats.  In get_state any pointer may be
- * NULL to skip that field.  The solver reorders storage every substep
+ * NULL to skip that field.  In set_state x, v, mass and inv_mass are
+ * required; x_star, lambda and level may be NULL (stepFrame overwrites them
+ * before reading them; without levels stepFrameWithLevels rejects the state).  The solver reorders storage every substep
  * (uniform_grid.hpp:102-105), exactly as the reference leaves the caller's
  * ParticleSet in the last substep's cell order. */
 int32_t apbf_gpu_set_state(apbf_gpu_solver* s, int32_t n, const float* x, const float* x_star,
@@ -185,13 +187,15 @@ int32_t apbf_gpu_last_phase_ms(const apbf_gpu_solver* s, float* out5);
 
 /* Per-launch CUDA-event timing of the two solver passes (lambda and
  * delta-p+apply), on the solver's own stream, accumulated over frames since
- * it was enabled; particle_iterations = sum of active particles over those
+ * the last call (each call resets the sums; switching on/off re-records the
+ * frame graph); particle_iterations = sum of active particles over those
  * launches (FrameStats.totalIterations).  Profiling hook, off by default. */
 int32_t apbf_gpu_set_kernel_timing(apbf_gpu_solver* s, int32_t enabled, apbf_error* err);
 int32_t apbf_gpu_kernel_times(const apbf_gpu_solver* s, double* lambda_ms, double* deltap_ms,
                               int64_t* launches, int64_t* particle_iterations);
 
-/* Number of kernels this library has launched so far (process-wide). */
+/* Number of kernels this library has launched so far (process-wide; the
+ * kernel nodes of every replayed frame graph included). */
 uint64_t apbf_gpu_launch_count(void);
 
 /* Sum of frozen-list lengths (incl. self) of the last substep and the

@@ -345,11 +345,26 @@ class ParticleSet:
 
 
 def _fp(a):
-    return a.ctypes.data_as(C.POINTER(C.c_float))
+    return None if a is None else a.ctypes.data_as(C.POINTER(C.c_float))
 
 
 def _ip(a):
-    return a.ctypes.data_as(C.POINTER(C.c_int32))
+    return None if a is None else a.ctypes.data_as(C.POINTER(C.c_int32))
+
+
+# stepFrame reads x, v, mass and inv_mass and overwrites x*, lambda and level
+# before reading them.  (Every field is an output: the frame reorders storage.)
+FRAME_INPUTS = ("x", "v", "mass", "inv_mass")
+
+
+def state_pointers(state, only=None):
+    """(x, x_star, v, mass, inv_mass, lambda_, level) pointers; fields not in
+    `only` (when given) are NULL."""
+    keep = lambda k: only is None or k in only  # noqa: E731
+    return (_fp(state.x if keep("x") else None), _fp(state.x_star if keep("x_star") else None),
+            _fp(state.v if keep("v") else None), _fp(state.mass if keep("mass") else None),
+            _fp(state.inv_mass if keep("inv_mass") else None),
+            _fp(state.lambda_ if keep("lambda_") else None), _ip(state.level if keep("level") else None))
 
 
 # ---------------------------------------------------------------- solver
@@ -414,15 +429,17 @@ class Solver:
         self._lib.apbf_gpu_set_iteration_observer(self._h, self._observer_c, None)
 
     # --- resident state ---
-    def upload(self, state: ParticleSet) -> None:
+    def upload(self, state: ParticleSet, frame_inputs_only: bool = False) -> None:
+        """apbf_gpu_set_state.  frame_inputs_only: upload just what stepFrame
+        reads (FRAME_INPUTS); step_frame_with_levels then needs a full upload."""
         state._normalise()
         err = capi.apbf_error()
-        rc = self._lib.apbf_gpu_set_state(self._h, state.count(), _fp(state.x), _fp(state.x_star),
-                                          _fp(state.v), _fp(state.mass), _fp(state.inv_mass),
-                                          _fp(state.lambda_), _ip(state.level), C.byref(err))
+        ptrs = state_pointers(state, FRAME_INPUTS if frame_inputs_only else None)
+        rc = self._lib.apbf_gpu_set_state(self._h, state.count(), *ptrs, C.byref(err))
         raise_for(rc, err)
 
     def download(self, state: ParticleSet) -> None:
+        """apbf_gpu_get_state (every field)."""
         n = self._lib.apbf_gpu_particle_count(self._h)
         if state.count() != n:
             state.x = np.zeros((n, 3), F32)
@@ -433,9 +450,7 @@ class Solver:
             state.lambda_ = np.zeros(n, F32)
             state.level = np.zeros(n, np.int32)
         err = capi.apbf_error()
-        rc = self._lib.apbf_gpu_get_state(self._h, _fp(state.x), _fp(state.x_star), _fp(state.v),
-                                          _fp(state.mass), _fp(state.inv_mass),
-                                          _fp(state.lambda_), _ip(state.level), C.byref(err))
+        rc = self._lib.apbf_gpu_get_state(self._h, *state_pointers(state), C.byref(err))
         raise_for(rc, err)
 
     def step_frame_resident(self, cam: Camera, lod_cfg: LodModelConfig, frame_index: int) -> FrameStats:

@@ -386,7 +386,10 @@ struct apbf_gpu_solver {
     double kt_lambda_ms = 0, kt_deltap_ms = 0;
     long long kt_launches = 0, kt_items = 0;
 
+    // Switching re-records the frame graph (the events are graph nodes);
+    // re-enabling while on only resets the accumulators (apbf_gpu_set_kernel_timing).
     void enable_kernel_timing(bool on) {
+        if (on == kernel_timing) return;
         drop_graph();
         eager_seen = false;
         kernel_timing = on;
@@ -855,6 +858,7 @@ struct apbf_gpu_solver {
     GraphKey gkey{}, seen_key{};
     cudaGraphExec_t gexec = nullptr;
     size_t kt_used_graph = 0;
+    unsigned long long graph_kernels = 0;  // kernel nodes of the frame graph
 
     GraphKey make_key(bool assign_lod, const apbf_camera* cam, const apbf_lod_config* lod) const {
         GraphKey k;
@@ -889,6 +893,7 @@ struct apbf_gpu_solver {
         cudaStream_t st = ws.stream;
         if (graphable && graph_ok && std::memcmp(&key, &gkey, sizeof key) == 0) {
             CK(cudaGraphLaunch(gexec, st));
+            g_launches += graph_kernels;
             cur = key.start ^ (cfg.substeps & 1);
             kt_used = kt_used_graph;
             CK(cudaStreamSynchronize(st));
@@ -898,6 +903,7 @@ struct apbf_gpu_solver {
             drop_graph();
             cudaGraph_t g = nullptr;
             CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+            const unsigned long long l0 = g_launches;
             capturing = true;
             try {
                 enqueue_frame(assign_lod, cam, lod);
@@ -909,12 +915,15 @@ struct apbf_gpu_solver {
                 throw;
             }
             CK(cudaStreamEndCapture(st, &g));
+            graph_kernels = g_launches - l0;  // captured, not run: counted per replay
+            g_launches = l0;
             CK(cudaGraphInstantiate(&gexec, g, 0));
             cudaGraphDestroy(g);
             kt_used_graph = kt_used;
             gkey = key;
             graph_ok = true;
             CK(cudaGraphLaunch(gexec, st));
+            g_launches += graph_kernels;
             cur = key.start ^ (cfg.substeps & 1);
             CK(cudaStreamSynchronize(st));
             return;
@@ -1085,23 +1094,40 @@ struct apbf_gpu_solver {
         destCountD.ensure(kMaxRanks);
         destStartD.ensure(kMaxRanks);
         minmax.ensure(2);
-        n = nloc;
         cur = 0;
-        levels_valid = true;
-        for (int i = 0; i < nloc; ++i)
-            levels_valid = levels_valid && level[i] >= cfg.n_min && level[i] <= cfg.n_max;
-        if (nloc == 0) return;
+        upload_state(nloc, x, xs, v, mass, inv_mass, lambda, level);
+    }
+
+    // Caller arrays go straight to the device staging area (DMA from the
+    // caller's memory: full PCIe rate when it is pinned), then one kernel
+    // unpacks them into the float4 SoA layout.  x_star, lambda and level may
+    // be NULL: stepFrame overwrites them before reading them (predict, the
+    // first iteration -- every level is >= nMin >= 1 -- and the LOD pass),
+    // so a caller that only steps frames need not upload them.  Without
+    // levels, stepFrameWithLevels reports them out of range.
+    void upload_state(int nn, const float* x, const float* xs, const float* v, const float* mass,
+                      const float* inv_mass, const float* lambda, const int32_t* level) {
+        n = nn;
+        levels_valid = level != nullptr || nn == 0;
+        if (nn == 0) return;
+        if (level) {  // branch-free so it vectorises (1M levels in ~0.1 ms)
+            const int lo = cfg.n_min, hi = cfg.n_max;
+            int bad = 0;
+            for (int i = 0; i < nn; ++i) bad |= (level[i] < lo) | (level[i] > hi);
+            levels_valid = bad == 0;
+        }
         cudaStream_t st = ws.stream;
         float* d = stage.p;
-        const size_t n1 = sizeof(float) * (size_t)nloc, n3 = 3 * n1;
+        const size_t n1 = sizeof(float) * (size_t)nn, n3 = 3 * n1;
         CK(cudaMemcpyAsync(d, x, n3, cudaMemcpyHostToDevice, st));
-        CK(cudaMemcpyAsync(d + 3LL * nloc, xs, n3, cudaMemcpyHostToDevice, st));
-        CK(cudaMemcpyAsync(d + 6LL * nloc, v, n3, cudaMemcpyHostToDevice, st));
-        CK(cudaMemcpyAsync(d + 9LL * nloc, mass, n1, cudaMemcpyHostToDevice, st));
-        CK(cudaMemcpyAsync(d + 10LL * nloc, inv_mass, n1, cudaMemcpyHostToDevice, st));
-        CK(cudaMemcpyAsync(d + 11LL * nloc, lambda, n1, cudaMemcpyHostToDevice, st));
-        CK(cudaMemcpyAsync(d + 12LL * nloc, level, n1, cudaMemcpyHostToDevice, st));
-        KL(k_unpack_state<<<blocks(nloc, 256), 256, 0, st>>>(nloc, d, set[0].view()));
+        if (xs) CK(cudaMemcpyAsync(d + 3LL * nn, xs, n3, cudaMemcpyHostToDevice, st));
+        CK(cudaMemcpyAsync(d + 6LL * nn, v, n3, cudaMemcpyHostToDevice, st));
+        CK(cudaMemcpyAsync(d + 9LL * nn, mass, n1, cudaMemcpyHostToDevice, st));
+        CK(cudaMemcpyAsync(d + 10LL * nn, inv_mass, n1, cudaMemcpyHostToDevice, st));
+        if (lambda) CK(cudaMemcpyAsync(d + 11LL * nn, lambda, n1, cudaMemcpyHostToDevice, st));
+        if (level) CK(cudaMemcpyAsync(d + 12LL * nn, level, n1, cudaMemcpyHostToDevice, st));
+        const int have = (xs ? 1 : 0) | (lambda ? 2 : 0) | (level ? 4 : 0);
+        KL(k_unpack_state<<<blocks(nn, 256), 256, 0, st>>>(nn, d, set[0].view(), have));
         LAUNCH_CHECK();
         CK(cudaStreamSynchronize(st));
     }
@@ -1589,29 +1615,11 @@ int32_t apbf_gpu_set_state(apbf_gpu_solver* s, int32_t n, const float* x, const 
     return guarded(err, [&] {
         if (n < 0) fail(APBF_ERR_INVALID_ARGUMENT, "negative particle count");
         CK(cudaSetDevice(s->ws.device));
+        if (n > 0 && (!x || !v || !mass || !inv_mass))
+            fail(APBF_ERR_INVALID_ARGUMENT, "x, v, mass and inv_mass are required");
         s->allocate(n);
         s->cur = 0;
-        s->levels_valid = true;
-        if (n == 0) return;
-        bool lv_ok = true;
-        for (int i = 0; i < n; ++i) lv_ok = lv_ok && level[i] >= s->cfg.n_min && level[i] <= s->cfg.n_max;
-        s->levels_valid = lv_ok;
-        // Caller arrays go straight to the device staging area (DMA from the
-        // caller's memory: full PCIe rate when it is pinned), then one kernel
-        // unpacks them into the float4 SoA layout.
-        cudaStream_t st = s->ws.stream;
-        float* d = s->stage.p;
-        const size_t n1 = sizeof(float) * (size_t)n, n3 = 3 * n1;
-        CK(cudaMemcpyAsync(d, x, n3, cudaMemcpyHostToDevice, st));
-        CK(cudaMemcpyAsync(d + 3LL * n, xs, n3, cudaMemcpyHostToDevice, st));
-        CK(cudaMemcpyAsync(d + 6LL * n, v, n3, cudaMemcpyHostToDevice, st));
-        CK(cudaMemcpyAsync(d + 9LL * n, mass, n1, cudaMemcpyHostToDevice, st));
-        CK(cudaMemcpyAsync(d + 10LL * n, inv_mass, n1, cudaMemcpyHostToDevice, st));
-        CK(cudaMemcpyAsync(d + 11LL * n, lambda, n1, cudaMemcpyHostToDevice, st));
-        CK(cudaMemcpyAsync(d + 12LL * n, level, n1, cudaMemcpyHostToDevice, st));
-        KL(k_unpack_state<<<blocks(n, 256), 256, 0, st>>>(n, d, s->set[0].view()));
-        LAUNCH_CHECK();
-        CK(cudaStreamSynchronize(st));
+        s->upload_state(n, x, xs, v, mass, inv_mass, lambda, level);
     });
 }
 
@@ -2037,12 +2045,16 @@ int32_t apbf_gpu_group_set_state(apbf_gpu_group* g, int32_t n, const float* x, c
         guarded(err, [] { fail(APBF_ERR_INVALID_ARGUMENT, "negative particle count"); });
         return APBF_ERR_INVALID_ARGUMENT;
     }
+    if (n > 0 && (!x || !v || !mass || !inv_mass)) {
+        guarded(err, [] { fail(APBF_ERR_INVALID_ARGUMENT, "x, v, mass and inv_mass are required"); });
+        return APBF_ERR_INVALID_ARGUMENT;
+    }
     const int G = (int)g->ranks.size();
     return group_run(g, err, [&](apbf_gpu_solver& s, int r) {
         // rank r takes the contiguous storage range [n r / G, n (r+1) / G)
         const long long b = (long long)n * r / G, e = (long long)n * (r + 1) / G;
-        s.set_state_local((int)(e - b), n, x + 3 * b, xs + 3 * b, v + 3 * b, mass + b, inv_mass + b,
-                          lambda + b, level + b);
+        s.set_state_local((int)(e - b), n, x + 3 * b, xs ? xs + 3 * b : nullptr, v + 3 * b, mass + b,
+                          inv_mass + b, lambda ? lambda + b : nullptr, level ? level + b : nullptr);
     });
 }
 

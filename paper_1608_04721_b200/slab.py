@@ -21,7 +21,7 @@ import numpy as np
 
 from . import capi
 from .api import (F32, Camera, FrameStats, LodModelConfig, ParticleSet, SdfScene, Solver,
-                  SolverConfig, _fp, _ip, raise_for)
+                  SolverConfig, FRAME_INPUTS, _fp, _ip, raise_for, state_pointers)
 
 
 def slab_partition(layer_hist: Sequence[int], nranks: int, min_layers: int = 2):
@@ -148,14 +148,12 @@ class SlabSolver(Solver):
         raise_for(self._lib.apbf_gpu_solver_attach_nccl(self._h, rank, nranks, buf, C.byref(err)), err)
         self.rank, self.nranks = rank, nranks
 
-    def upload_slice(self, state: ParticleSet, n_global: int) -> None:
+    def upload_slice(self, state: ParticleSet, n_global: int, frame_inputs_only: bool = False) -> None:
         """This rank's contiguous slice of the global storage order."""
         state._normalise()
         err = capi.apbf_error()
-        rc = self._lib.apbf_gpu_slab_set_state(self._h, state.count(), n_global, _fp(state.x),
-                                               _fp(state.x_star), _fp(state.v), _fp(state.mass),
-                                               _fp(state.inv_mass), _fp(state.lambda_),
-                                               _ip(state.level), C.byref(err))
+        ptrs = state_pointers(state, FRAME_INPUTS if frame_inputs_only else None)
+        rc = self._lib.apbf_gpu_slab_set_state(self._h, state.count(), n_global, *ptrs, C.byref(err))
         raise_for(rc, err)
 
 

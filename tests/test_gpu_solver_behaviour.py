@@ -276,3 +276,30 @@ def test_tier_b_float_gpu_vs_reference_double():
     e_ref = tree.query(d32.x)[0].max()
     assert e_gpu <= 2 * e_ref + 1e-7
     assert e_gpu < 0.0125  # well below the lattice spacing 0.025
+
+
+def test_frame_inputs_only_upload_matches_full_upload():
+    """x*, lambda and level are dead inputs of stepFrame: uploading only x, v,
+    mass and inv_mass (the e2e bench path) gives the same frames bit for bit,
+    and stepFrameWithLevels refuses a state uploaded without levels."""
+    spec = S.build_scenario("dam_break", 8000 / 216000)
+    spec.lod.model = LodModel.DTVS
+    a = S.make_state(spec, 3)
+    rng = np.random.default_rng(0)
+    a.x_star[:] = rng.normal(size=a.x_star.shape)  # garbage the frame must not read
+    a.lambda_[:] = rng.normal(size=a.lambda_.shape)
+    b = a.copy()
+    full, part = Solver(spec.solver, spec.scene), Solver(spec.solver, spec.scene)
+    for f in range(3):
+        full.upload(a)
+        part.upload(b, frame_inputs_only=True)
+        sa = full.step_frame_resident(spec.camera, spec.lod, f)
+        sb = part.step_frame_resident(spec.camera, spec.lod, f)
+        assert (sa.total_iterations, sa.min_density_pct) == (sb.total_iterations, sb.min_density_pct)
+        full.download(a)
+        part.download(b)
+        for k in ("x", "x_star", "v", "mass", "inv_mass", "lambda_", "level"):
+            assert np.array_equal(getattr(a, k), getattr(b, k)), (f, k)
+    part.upload(b, frame_inputs_only=True)
+    with pytest.raises(ValueError):
+        part.step_frame_with_levels_resident(0)

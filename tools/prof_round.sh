@@ -3,6 +3,6 @@ python bench.py --steps 20 --warmup 5 > gpurun_out/bench_n1.json 2> gpurun_out/b
 cat gpurun_out/bench_n1.json
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/ncu_l.log 2>&1
 for k in k_lambda k_deltap_apply k_build_lists; do
-ncu --set full --clock-control none --import-source on -k regex:$k --launch-skip 41 --launch-count 1 -o gpurun_out/prof_$k -f python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/ncu_$k.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:$k --launch-skip $([ $k = k_build_lists ] && echo 5 || echo 41) --launch-count 1 -o gpurun_out/prof_$k -f python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/ncu_$k.log 2>&1
 done
 ls -la gpurun_out
