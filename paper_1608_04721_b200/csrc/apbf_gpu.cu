@@ -506,6 +506,7 @@ struct apbf_gpu_solver {
         volatile float sh = sc.kc.spiky * sc.kc.h;
         volatile float shh = sh * sc.kc.h;
         sc.fastDiv = (cfg.h > 0.0f && cfg.h <= 0x1p60f && sc.kc.spiky < 0.0f && -shh < 0x1p61f) ? 1 : 0;
+        sc.w0 = w0;
         return sc;
     }
 
@@ -514,6 +515,10 @@ struct apbf_gpu_solver {
     // delta-p pass recompute the spiky coefficients instead of reading the
     // lambda pass's cache.  Every variant is bit-identical.
     bool use_stage = false, use_coef = true, use_tiles = false;
+    // every particle has the same inverse mass w0 (bitwise; checked at upload,
+    // frames only permute it); single-GPU only -- a slab rank cannot see its ghosts'
+    bool uniform_w = false;
+    float w0 = 0.0f;
     bool use_c16 = false;  // APBF_C16=1: compact 16-bit lists (slower here: the passes are latency-bound)
     int block_threads = 128;  // APBF_BLOCK: CTA size of the order-based passes
     int chunk = 4;            // APBF_CHUNK: neighbours gathered per batch (1, 2, 4, 8)
@@ -527,9 +532,21 @@ struct apbf_gpu_solver {
         Ctl* ctl = ws.ctl.p;
         const int sb = blocks(n_iter, kBT);
         const int smem = kS ? kSolverSmem : 0;
-        KL(k_lambda<kS, kC, kBT, kK, kZ><<<sb, kBT, smem, st>>>(n_iter, it, ctl, activeCount.p, order.p, Pc,
-                                                             dst.W, dst.L, nbr.p, nbrCount.p, groupBase.p,
-                                                             coef.p, sc, s, ownB_, ownE_, PL.p));
+        // uniform inverse mass: specialised lambda only for the default variant
+        if constexpr (!kS && kC && kK == 4) {
+            if (uniform_w)
+                KL(k_lambda<kS, kC, kBT, kK, kZ, true><<<sb, kBT, smem, st>>>(
+                    n_iter, it, ctl, activeCount.p, order.p, Pc, dst.W, dst.L, nbr.p, nbrCount.p,
+                    groupBase.p, coef.p, sc, s, ownB_, ownE_, PL.p));
+            else
+                KL(k_lambda<kS, kC, kBT, kK, kZ><<<sb, kBT, smem, st>>>(
+                    n_iter, it, ctl, activeCount.p, order.p, Pc, dst.W, dst.L, nbr.p, nbrCount.p,
+                    groupBase.p, coef.p, sc, s, ownB_, ownE_, PL.p));
+        } else {
+            KL(k_lambda<kS, kC, kBT, kK, kZ><<<sb, kBT, smem, st>>>(n_iter, it, ctl, activeCount.p, order.p, Pc,
+                                                                 dst.W, dst.L, nbr.p, nbrCount.p, groupBase.p,
+                                                                 coef.p, sc, s, ownB_, ownE_, PL.p));
+        }
         if (tslot >= 0) rec(kt_ev[tslot][1]);
         KL(k_deltap_apply<kZ, kS, kC, kBT, kK><<<sb, kBT, smem, st>>>(
             n_iter, it, ctl, activeCount.p, order.p, Pc, Pn, dst.W, dst.L, dst.LV, nbr.p, nbrCount.p,
@@ -869,7 +886,8 @@ struct apbf_gpu_solver {
         k.ktime = kernel_timing;
         k.ptime = phase_timing;
         k.n = n;
-        k.flags = (use_tiles ? 1 : 0) | (use_stage ? 2 : 0) | (use_coef ? 4 : 0) | (use_c16 ? 8 : 0) | (chunk << 4) |
+        k.flags = (use_tiles ? 1 : 0) | (use_stage ? 2 : 0) | (use_coef ? 4 : 0) | (use_c16 ? 8 : 0) |
+                  (uniform_w ? 0x100000 : 0) | (chunk << 4) |
                   (block_threads << 8);
         k.caps[0] = nbrCap;
         k.caps[1] = listCap16;
@@ -1115,6 +1133,14 @@ struct apbf_gpu_solver {
             int bad = 0;
             for (int i = 0; i < nn; ++i) bad |= (level[i] < lo) | (level[i] > hi);
             levels_valid = bad == 0;
+        }
+        uniform_w = false;
+        if (!transport && inv_mass) {
+            unsigned diff = 0;
+            const unsigned* b = reinterpret_cast<const unsigned*>(inv_mass);
+            for (int i = 1; i < nn; ++i) diff |= b[i] ^ b[0];
+            uniform_w = diff == 0;
+            w0 = inv_mass[0];
         }
         cudaStream_t st = ws.stream;
         float* d = stage.p;

@@ -65,3 +65,24 @@ def test_multi_dam_break_cone_bitwise():
     """Cone SDF (glibc hypotf reproduced on the device) + box."""
     spec = S.build_scenario("multi_dam_break", 0.1)
     run_pair(spec, 4)
+
+
+@pytest.mark.parametrize("uniform", [True, False])
+def test_mass_distribution_bitwise(uniform):
+    """Uniform inverse mass takes the lambda variant that does not gather w_j;
+    varied masses (and some static w = 0 particles) take the general one."""
+    spec = S.build_scenario("dam_break", 8000 / 216000)
+    spec.lod.model = LodModel.DTVS
+    gpu = Solver(spec.solver, spec.scene)
+    orc = OracleSolver(spec.solver, spec.scene)
+    a = S.make_state(spec, 5)
+    if not uniform:
+        rng = np.random.default_rng(7)
+        a.mass[:] = (a.mass * rng.uniform(0.5, 2.0, a.mass.shape)).astype(np.float32)
+        a.inv_mass[:] = (np.float32(1) / a.mass).astype(np.float32)
+        a.inv_mass[::17] = 0  # pinned particles
+    b = a.copy()
+    for f in range(4):
+        gpu.step_frame(a, spec.camera, spec.lod, f)
+        orc.step_frame(b, spec.camera, spec.lod, f)
+        assert_same_state(a, b, f"frame {f}")
