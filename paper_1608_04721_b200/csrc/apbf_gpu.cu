@@ -455,8 +455,10 @@ struct apbf_gpu_solver {
         nbrCount.ensure(groups * 32);
         groupBase.ensure(groups);
         lbase.ensure(groups * 32);
-        if (nbrCap < (long long)m * 48 + 4096) {
-            nbrCap = (long long)m * 48 + 4096;
+        list_groups = (long long)groups;
+        const long long need = use_c16 ? (long long)m * 48 + 4096 : list_groups * list_stride * 32;
+        if (nbrCap < need) {
+            nbrCap = need;
             alloc_lists();
         }
         numTiles = (int)((m + kTileSize - 1) / kTileSize);
@@ -519,7 +521,11 @@ struct apbf_gpu_solver {
     // frames only permute it); single-GPU only -- a slab rank cannot see its ghosts'
     bool uniform_w = false;
     float w0 = 0.0f;
-    bool use_c16 = false;  // APBF_C16=1: compact 16-bit lists (slower here: the passes are latency-bound)
+    bool use_c16 = false;
+    // 32-bit lists: rows per lane of every warp slab (k_build_lists_direct);
+    // grows on overflow, never shrinks
+    int list_stride = 64;
+    long long list_groups = 0;  // APBF_C16=1: compact 16-bit lists (slower here: the passes are latency-bound)
     int block_threads = 128;  // APBF_BLOCK: CTA size of the order-based passes
     int chunk = 4;            // APBF_CHUNK: neighbours gathered per batch (1, 2, 4, 8)
     int ownB_ = 0, ownE_ = 0x7fffffff;  // owned slot range (slab mode); everything otherwise
@@ -582,9 +588,9 @@ struct apbf_gpu_solver {
                 nn, ws.ctl.p, order.p, dst.XS, ws.cellCount.p, cfg.h, cfg.h * cfg.h, nbr.p, nbrCount.p,
                 groupBase.p, nbrCap, nbr16.p, lbase.p));
         else
-            KL(k_build_lists<false><<<blocks(nn, kListThreads), kListThreads, 0, st>>>(
+            KL(k_build_lists_direct<<<blocks(nn, kListThreads), kListThreads, 0, st>>>(
                 nn, ws.ctl.p, order.p, dst.XS, ws.cellCount.p, cfg.h, cfg.h * cfg.h, nbr.p, nbrCount.p,
-                groupBase.p, nbrCap, nbr16.p, lbase.p));
+                groupBase.p, list_stride));
     }
     void launch_residual(int nn, int it, const float4* Pn, const SolverConsts& sc, double* out, int oB,
                          int oE) {
@@ -706,7 +712,9 @@ struct apbf_gpu_solver {
         const int why = ws.h_ctl->list_overflow;
         if (!use_tiles) {
             if (why & 2) use_c16 = false;
-            if (why & 1) nbrCap = std::max<long long>(nbrCap * 2, (long long)(used * 3 / 2));
+            if ((why & 1) && use_c16) nbrCap = std::max<long long>(nbrCap * 2, (long long)(used * 3 / 2));
+            if ((why & 1) && !use_c16) list_stride = std::max(list_stride + 16, (int)used_fb + 8);
+            if (!use_c16) nbrCap = std::max(nbrCap, list_groups * list_stride * 32);
             alloc_lists();
             return;
         }

@@ -75,3 +75,27 @@ def test_compact_lists_fall_back_when_offsets_overflow(monkeypatch):
     Solver(cfg).step_frame_with_levels(b, 0)
     for k in FIELDS:
         assert np.array_equal(getattr(a, k), getattr(b, k)), k
+
+
+def test_dense_cluster_widens_list_stride():
+    """Spacing h/4 gives ~270 neighbours per particle, far past the initial
+    64-row slab stride: the build flags the overflow, the host widens the
+    stride and re-runs the frame, which must still match the oracle."""
+    from oracle.oracle import OracleSolver
+    h = 0.1
+    side = 14
+    g = np.stack(np.meshgrid(*[np.arange(side)] * 3, indexing="ij"), -1).reshape(-1, 3)
+    x = (g * (h / 4) + 0.5).astype(np.float32)
+    cfg = S.build_scenario("dam_break", 0.01).solver
+    cfg.h = h
+    cfg.range = IterationRange(2, 3)
+    a = ParticleSet(x, 0.002, 3)
+    b = a.copy()
+    gpu = Solver(cfg)
+    sa = gpu.step_frame_with_levels(a, 0)
+    sb = OracleSolver(cfg).step_frame_with_levels(b, 0)
+    assert sa.total_iterations == sb.total_iterations
+    for k in FIELDS:
+        assert np.array_equal(getattr(a, k), getattr(b, k)), k
+    entries, _ = gpu.last_neighbor_stats()
+    assert entries / a.count() > 100
