@@ -282,6 +282,19 @@ int32_t apbf_gpu_lod_dtvs(int32_t n, const float* positions, const apbf_camera* 
 int32_t apbf_gpu_splat(int32_t n, const float* positions, float radius, const apbf_camera* cam,
                        float* depth_out, apbf_error* err);
 
+/* renderLevelImage (depth_splat.hpp:314-350): opaque splat render, each
+ * pixel coloured by the level of its nearest particle (ties: lowest index)
+ * with levelColor (:296-310); rgb_out holds width*height*3 bytes, row-major,
+ * black where nothing was hit -- the ImageRgb that writePpm (:251-262)
+ * stores.  Runs on the device; only the image is downloaded. */
+int32_t apbf_gpu_render_level_image(int32_t n, const float* positions, const int32_t* levels, float radius,
+                                    const apbf_camera* cam, int32_t n_min, int32_t n_max, uint8_t* rgb_out,
+                                    apbf_error* err);
+/* The same for the solver's resident state (x and level, storage order);
+ * runScenario's frame_XXXXXX.ppm dumps (runner.cpp:85-90). */
+int32_t apbf_gpu_render_levels(apbf_gpu_solver* s, const apbf_camera* cam, float radius, int32_t n_min,
+                               int32_t n_max, uint8_t* rgb_out, apbf_error* err);
+
 /* findContacts(...).size() (sdf.hpp:226-250). */
 int32_t apbf_gpu_count_contacts(int32_t n, const float* positions, const apbf_sdf_primitive* prims,
                                 int32_t n_prims, float gradient_step, float radius,

@@ -373,6 +373,17 @@ def rlib():
             "ref_build_scenario": (C.c_int32, [C.c_char_p, C.c_double, C.c_uint64,
                                                C.POINTER(ref_scenario), _dp, E]),
             "ref_splitmix64_first": (C.c_uint64, [C.c_uint64]),
+            "ref_render_level_image": (C.c_int32, [C.c_int32, C.c_int32, _dp, _ip, C.c_double,
+                                                   C.POINTER(ref_camera), C.c_int32, C.c_int32,
+                                                   C.POINTER(C.c_uint8), E]),
+            "ref_write_particle_snapshot": (C.c_int32, [C.c_int32, C.c_int32, _dp, _ip, C.c_char_p, E]),
+            "ref_run_scenario": (C.c_int32, [C.c_char_p, C.c_double, C.c_int32, C.c_int32, C.c_int32,
+                                             C.c_int32, C.c_int32, C.c_uint64, C.c_int32, C.c_char_p,
+                                             C.c_int32, C.c_int32, E]),
+            "ref_format_bench_report": (C.c_int32, [C.c_int32, C.POINTER(C.c_char_p), _dp,
+                                                    C.POINTER(C.c_int64), _ip, _ip, C.c_char_p, C.c_int32,
+                                                    E]),
+            "ref_parse_bench_mode": (C.c_int32, [C.c_char_p, _ip, _ip, _ip, E]),
         }
         for k, (r, a) in sig.items():
             f = getattr(L, k)
@@ -601,6 +612,68 @@ def ref_splat(positions, r, cam: Camera, prec=4):
     rc = L.ref_splat(prec, p.shape[0], dp(p), r, C.byref(ref_cam(cam)), dp(out), C.byref(err))
     _rraise(rc, err)
     return out.reshape(cam.height, cam.width)
+
+
+def ref_render_level_image(positions, levels, r, cam: Camera, nmin, nmax, prec=4):
+    """renderLevelImage<S> of the reference: (height, width, 3) uint8."""
+    L = rlib()
+    p = np.ascontiguousarray(positions, np.float64).reshape(-1, 3)
+    lv = np.ascontiguousarray(levels, np.int32)
+    out = np.zeros(cam.width * cam.height * 3, np.uint8)
+    err = ref_error()
+    rc = L.ref_render_level_image(prec, p.shape[0], dp(p), lv.ctypes.data_as(C.POINTER(C.c_int32)), r,
+                                  C.byref(ref_cam(cam)), nmin, nmax,
+                                  out.ctypes.data_as(C.POINTER(C.c_uint8)), C.byref(err))
+    _rraise(rc, err)
+    return out.reshape(cam.height, cam.width, 3)
+
+
+def ref_write_particle_snapshot(path, positions, levels, prec=4):
+    L = rlib()
+    p = np.ascontiguousarray(positions, np.float64).reshape(-1, 3)
+    lv = np.ascontiguousarray(levels, np.int32)
+    err = ref_error()
+    rc = L.ref_write_particle_snapshot(prec, p.shape[0], dp(p), lv.ctypes.data_as(C.POINTER(C.c_int32)),
+                                       str(path).encode(), C.byref(err))
+    _rraise(rc, err)
+
+
+def ref_run_scenario(name, scale, mode, out_dir, frames, seed=0, lod=-1, rng=None, deterministic=True,
+                     images_every=0, particles_every=0):
+    """The reference's own runScenario (Solver<double>), writing into out_dir."""
+    L = rlib()
+    err = ref_error()
+    nmin, nmax = (rng.n_min, rng.n_max) if rng is not None else (0, 0)
+    rc = L.ref_run_scenario(name.encode(), scale, mode, lod, nmin, nmax, frames, seed, int(deterministic),
+                            str(out_dir).encode(), images_every, particles_every, C.byref(err))
+    _rraise(rc, err)
+
+
+def ref_format_bench_report(results):
+    """formatBenchReport of [(token, median_ms, iterations, frames, particles)]."""
+    L = rlib()
+    k = len(results)
+    toks = (C.c_char_p * k)(*[r[0].encode() for r in results])
+    med = np.array([r[1] for r in results], np.float64)
+    its = (C.c_int64 * k)(*[r[2] for r in results])
+    fr = np.array([r[3] for r in results], np.int32)
+    pa = np.array([r[4] for r in results], np.int32)
+    buf = C.create_string_buffer(1 << 16)
+    err = ref_error()
+    rc = L.ref_format_bench_report(k, toks, dp(med), its, fr.ctypes.data_as(C.POINTER(C.c_int32)),
+                                   pa.ctypes.data_as(C.POINTER(C.c_int32)), buf, len(buf), C.byref(err))
+    _rraise(rc, err)
+    return buf.value.decode()
+
+
+def ref_parse_bench_mode(token):
+    """(mode, iterations, lod) or ValueError(message) like parseBenchMode."""
+    L = rlib()
+    m, it, lod = C.c_int32(), C.c_int32(), C.c_int32()
+    err = ref_error()
+    rc = L.ref_parse_bench_mode(token.encode(), C.byref(m), C.byref(it), C.byref(lod), C.byref(err))
+    _rraise(rc, err)
+    return m.value, it.value, lod.value
 
 
 def ref_scene_distance(scene: SdfScene, point, prec=4):

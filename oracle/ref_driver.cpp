@@ -19,6 +19,9 @@
 #include <string>
 
 #include "apbf/solver.hpp"
+#include "bench.hpp"
+#include "metrics.hpp"
+#include "runner.hpp"
 #include "scenario.hpp"
 
 #ifdef _OPENMP
@@ -496,6 +499,91 @@ int32_t ref_build_scenario(const char* name, double scale, uint64_t seed, ref_sc
         const ParticleSet<double> st = makeState(spec, seed);
         out->mass = st.mass.size() > 0 ? st.mass[0] : 0.0;
         if (positions) from_mat3(st.x, positions);
+    });
+}
+
+// renderLevelImage<S> (depth_splat.hpp:314-350) -> width*height*3 bytes.
+int32_t ref_render_level_image(int32_t prec, int32_t n, const double* pos, const int32_t* levels,
+                               double radius, const ref_camera* cam, int32_t nmin, int32_t nmax,
+                               uint8_t* rgb, ref_error* err) {
+    return guarded(err, [&] {
+        auto run = [&](auto tag) {
+            using S = decltype(tag);
+            VecXi lv(n);
+            for (int i = 0; i < n; ++i) lv[i] = levels[i];
+            const ImageRgb img = renderLevelImage(to_mat3<S>(n, pos), lv, S(radius), to_cam<S>(*cam),
+                                                  IterationRange(nmin, nmax));
+            std::memcpy(rgb, img.rgb.data(), img.rgb.size());
+        };
+        if (prec == 4) run(float{});
+        else run(double{});
+    });
+}
+
+// writeParticleSnapshot<S> (particle_state.hpp:148-167) of n particles.
+int32_t ref_write_particle_snapshot(int32_t prec, int32_t n, const double* pos, const int32_t* levels,
+                                    const char* path, ref_error* err) {
+    return guarded(err, [&] {
+        auto run = [&](auto tag) {
+            using S = decltype(tag);
+            ParticleSet<S> st(to_mat3<S>(n, pos), S(1), 1);
+            for (int i = 0; i < n; ++i) st.level[i] = levels[i];
+            writeParticleSnapshot(std::filesystem::path(path), st);
+        };
+        if (prec == 4) run(float{});
+        else run(double{});
+    });
+}
+
+// runScenario (runner.cpp:60-98) -- the reference's own harness, Solver<double>.
+// lod: -1 keep the scenario's, 0 dtc, 1 dtvs; nmin 0 = keep the range.
+int32_t ref_run_scenario(const char* name, double scale, int32_t mode, int32_t lod, int32_t nmin,
+                         int32_t nmax, int32_t frames, uint64_t seed, int32_t deterministic,
+                         const char* out_dir, int32_t images_every, int32_t particles_every,
+                         ref_error* err) {
+    return guarded(err, [&] {
+        const ScenarioSpec spec = buildScenario(name, scale);
+        RunOptions opt;
+        opt.mode = mode == 0 ? SolverMode::Pbf : SolverMode::Apbf;
+        if (lod >= 0) opt.lodModel = lod == 0 ? LodModel::Dtc : LodModel::Dtvs;
+        if (nmin > 0) opt.range = IterationRange(nmin, nmax);
+        opt.frames = frames;
+        opt.seed = seed;
+        opt.deterministic = deterministic != 0;
+        opt.outDir = out_dir ? out_dir : "";
+        opt.dumpImagesEvery = images_every;
+        opt.dumpParticlesEvery = particles_every;
+        (void)runScenario(spec, opt);
+    });
+}
+
+// formatBenchReport (bench.cpp:93-123) of caller-made results.
+int32_t ref_format_bench_report(int32_t k, const char* const* tokens, const double* median_ms,
+                                const int64_t* iterations, const int32_t* frames,
+                                const int32_t* particles, char* out, int32_t cap, ref_error* err) {
+    return guarded(err, [&] {
+        std::vector<BenchResult> rs(static_cast<size_t>(k));
+        for (int i = 0; i < k; ++i) {
+            rs[size_t(i)].token = tokens[i];
+            rs[size_t(i)].medianFrameMs = median_ms[i];
+            rs[size_t(i)].iterations = iterations[i];
+            rs[size_t(i)].frames = frames[i];
+            rs[size_t(i)].particles = particles[i];
+        }
+        const std::string s = formatBenchReport(rs);
+        std::snprintf(out, size_t(cap), "%s", s.c_str());
+    });
+}
+
+// parseBenchMode (bench.cpp:9-42): 0 ok (mode, iterations, lod -1/0/1), or
+// the invalid_argument message in err.
+int32_t ref_parse_bench_mode(const char* token, int32_t* mode, int32_t* iters, int32_t* lod,
+                             ref_error* err) {
+    return guarded(err, [&] {
+        const BenchMode m = parseBenchMode(token);
+        *mode = m.mode == SolverMode::Pbf ? 0 : 1;
+        *iters = m.pbfIterations;
+        *lod = m.lodModel ? (*m.lodModel == LodModel::Dtc ? 0 : 1) : -1;
     });
 }
 

@@ -453,6 +453,15 @@ class Solver:
         rc = self._lib.apbf_gpu_get_state(self._h, *state_pointers(state), C.byref(err))
         raise_for(rc, err)
 
+    def render_levels(self, cam: Camera, r: float, rng: IterationRange) -> np.ndarray:
+        """renderLevelImage of the resident state (x, level) on the device."""
+        out = np.zeros(max(1, cam.width * cam.height * 3), np.uint8)
+        err = capi.apbf_error()
+        rc = self._lib.apbf_gpu_render_levels(self._h, C.byref(cam.to_c()), r, rng.n_min, rng.n_max,
+                                              out.ctypes.data_as(C.POINTER(C.c_uint8)), C.byref(err))
+        raise_for(rc, err)
+        return out.reshape(cam.height, cam.width, 3)
+
     def step_frame_resident(self, cam: Camera, lod_cfg: LodModelConfig, frame_index: int) -> FrameStats:
         st = capi.apbf_frame_stats()
         st.residuals = self._res
@@ -632,6 +641,49 @@ def splat(positions, r: float, cam: Camera) -> np.ndarray:
     rc = lib.apbf_gpu_splat(p.shape[0], _fp(p), r, C.byref(cam.to_c()), _fp(out), C.byref(err))
     raise_for(rc, err)
     return out.reshape(cam.height, cam.width)
+
+
+def render_level_image(positions, levels, r: float, cam: Camera, rng: IterationRange) -> np.ndarray:
+    """renderLevelImage (depth_splat.hpp:314-350) on the device: (height,
+    width, 3) uint8, each pixel the levelColor of its nearest particle."""
+    lib = capi.lib()
+    p = _pos(positions)
+    lv = np.ascontiguousarray(levels, np.int32)
+    if lv.shape[0] != p.shape[0]:
+        raise ValueError("level array size mismatch")
+    out = np.zeros(max(1, cam.width * cam.height * 3), np.uint8)
+    err = capi.apbf_error()
+    rc = lib.apbf_gpu_render_level_image(p.shape[0], _fp(p), _ip(lv), r, C.byref(cam.to_c()), rng.n_min,
+                                         rng.n_max, out.ctypes.data_as(C.POINTER(C.c_uint8)), C.byref(err))
+    raise_for(rc, err)
+    return out.reshape(cam.height, cam.width, 3)
+
+
+def write_ppm(image: np.ndarray, path) -> None:
+    """writePpm (depth_splat.hpp:251-262): binary P6."""
+    h, w, _ = image.shape
+    with open(path, "wb") as f:
+        f.write(f"P6\n{w} {h}\n255\n".encode())
+        f.write(np.ascontiguousarray(image, np.uint8).tobytes())
+
+
+def read_ppm(path) -> np.ndarray:
+    with open(path, "rb") as f:
+        data = f.read()
+    parts = data.split(b"\n", 3)
+    if parts[0] != b"P6" or parts[2] != b"255":
+        raise ValueError(f"{path}: not a P6/255 image")
+    w, h = (int(v) for v in parts[1].split())
+    return np.frombuffer(parts[3], np.uint8, count=w * h * 3).reshape(h, w, 3)
+
+
+def write_particle_snapshot(path, state: ParticleSet) -> None:
+    """writeParticleSnapshot (particle_state.hpp:148-167): x,y,z,level per
+    particle, coordinates as %.17g of their (float) values."""
+    with open(path, "w") as f:
+        f.write("x,y,z,level\n")
+        x = state.x.astype(np.float64)
+        f.writelines(f"{a:.17g},{b:.17g},{c:.17g},{int(lv)}\n" for (a, b, c), lv in zip(x, state.level))
 
 
 def count_contacts(scene: SdfScene, positions, r: float) -> int:

@@ -141,6 +141,9 @@ struct Workspace {
     DBuf<float> dist;
     DBuf<unsigned> keys;
     DBuf<float4> tmp4;
+    DBuf<unsigned long long> owner;  // renderLevelImage: (depth bits, index) per pixel
+    DBuf<unsigned char> rgb;
+    DBuf<int> tmpi;
 
     explicit Workspace(int dev) : device(dev) {
         CK(cudaSetDevice(dev));
@@ -323,6 +326,24 @@ Workspace& component_ws() {
     if ((int)v.size() <= dev) v.resize(dev + 1, nullptr);
     if (!v[dev]) v[dev] = new Workspace(dev);
     return *v[dev];
+}
+
+// renderLevelImage (depth_splat.hpp:314-350) of n device positions/levels
+// into the caller's width*height*3 bytes.
+void render_levels(Workspace& ws, int n, const float4* X, const int* LV, float radius, const apbf_camera& cam,
+                   int nMin, int nMax, unsigned char* rgb_out) {
+    if (!(radius > 0.0f)) fail(APBF_ERR_INVALID_ARGUMENT, "splat radius must be positive");
+    const CamFrame f = make_frame(cam);
+    const int px = cam.width * cam.height;
+    ws.owner.ensure((size_t)px);
+    ws.rgb.ensure((size_t)px * 3);
+    cudaStream_t st = ws.stream;
+    CK(cudaMemsetAsync(ws.owner.p, 0xff, sizeof(unsigned long long) * px, st));
+    if (n > 0) KL(k_render_splat<<<blocks(n, 256), 256, 0, st>>>(n, X, radius, f, ws.owner.p));
+    KL(k_render_color<<<blocks(px, 256), 256, 0, st>>>(px, ws.owner.p, LV, nMin, nMax, ws.rgb.p));
+    LAUNCH_CHECK();
+    CK(cudaMemcpyAsync(rgb_out, ws.rgb.p, (size_t)px * 3, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
 }
 
 void upload_pos4(Workspace& ws, int n, const float* pos, const float* mass = nullptr) {
@@ -1966,6 +1987,30 @@ int32_t apbf_gpu_splat(int32_t n, const float* positions, float radius, const ap
         LAUNCH_CHECK();
         CK(cudaMemcpyAsync(depth_out, ws.depth.p, sizeof(float) * px, cudaMemcpyDeviceToHost, ws.stream));
         CK(cudaStreamSynchronize(ws.stream));
+    });
+}
+
+int32_t apbf_gpu_render_level_image(int32_t n, const float* positions, const int32_t* levels, float radius,
+                                    const apbf_camera* cam, int32_t n_min, int32_t n_max, uint8_t* rgb_out,
+                                    apbf_error* err) {
+    return guarded(err, [&] {
+        Workspace& ws = component_ws();
+        if (n > 0) {
+            upload_pos4(ws, n, positions);
+            ws.tmpi.ensure((size_t)n);
+            CK(cudaMemcpyAsync(ws.tmpi.p, levels, sizeof(int) * n, cudaMemcpyHostToDevice, ws.stream));
+        }
+        render_levels(ws, n, ws.tmp4.p, ws.tmpi.p, radius, *cam, n_min, n_max, rgb_out);
+    });
+}
+
+int32_t apbf_gpu_render_levels(apbf_gpu_solver* s, const apbf_camera* cam, float radius, int32_t n_min,
+                               int32_t n_max, uint8_t* rgb_out, apbf_error* err) {
+    return guarded(err, [&] {
+        if (s->transport) fail(APBF_ERR_INVALID_ARGUMENT, "render_levels needs the whole state on one rank");
+        CK(cudaSetDevice(s->ws.device));
+        render_levels(s->ws, s->n, s->set[s->cur].X.p, s->set[s->cur].LV.p, radius, *cam, n_min, n_max,
+                      rgb_out);
     });
 }
 

@@ -83,10 +83,69 @@ def scenario_case():
     np.savez_compressed(os.path.join(OUT, "scenarios.npz"), **out)
 
 
+def harness_case():
+    """The reference's own harness outputs (runner/metrics/bench): metrics.csv
+    of runScenario (Solver<double>), the frame dumps that renderLevelImage<float>
+    and writeParticleSnapshot<float> make of the reference Solver<float> state,
+    formatBenchReport / parseBenchMode answers."""
+    import json
+    import tempfile
+    out = {}
+    with tempfile.TemporaryDirectory() as d:
+        # C1-like dam break, 10 deterministic frames, DTVS (the scenario default)
+        O.ref_run_scenario("dam_break", 8000 / 216000, 1, d, 10, seed=1)
+        out["metrics_dam_apbf"] = np.array([open(os.path.join(d, "metrics.csv")).read()])
+    with tempfile.TemporaryDirectory() as d:
+        O.ref_run_scenario("dam_break", 8000 / 216000, 0, d, 4, seed=1, rng=IterationRange(3, 3))
+        out["metrics_dam_pbf3"] = np.array([open(os.path.join(d, "metrics.csv")).read()])
+    # dumps of the float reference after 2 frames of dam_break(0.001), seed 11
+    spec = S.build_scenario("dam_break", 0.001)
+    st = S.make_state(spec, 11)
+    rs = O.RefState.from_set(st)
+    sv = O.RefSolver(spec.solver, spec.scene, prec=4)
+    for f in range(2):
+        sv.step_frame(rs, spec.camera, spec.lod, f)
+    r = float(np.float32(spec.solver.h) / np.float32(4))
+    img = O.ref_render_level_image(rs.x, rs.level, r, spec.camera, spec.solver.range.n_min,
+                                   spec.solver.range.n_max, prec=4)
+    with tempfile.TemporaryDirectory() as d:
+        path = os.path.join(d, "p.csv")
+        O.ref_write_particle_snapshot(path, rs.x, rs.level, prec=4)
+        out["snapshot_dam_f1"] = np.array([open(path).read()])
+    out["image_dam_f1"] = img
+    out["state_dam_f1_x"] = rs.x.astype(np.float32)
+    out["state_dam_f1_level"] = rs.level.astype(np.int32)
+    # a wider render: the dam_break(8000) initial lattice with mixed levels
+    spec8 = S.build_scenario("dam_break", 8000 / 216000)
+    x8 = S.spawn_scenario(spec8, 1).astype(np.float32)
+    lv8 = (3 + (np.arange(x8.shape[0]) * 7919) % 4).astype(np.int32)
+    out["render_x"] = x8
+    out["render_level"] = lv8
+    out["render_image"] = O.ref_render_level_image(x8, lv8, 0.0125, spec8.camera, 3, 6, prec=4)
+    reports = [
+        [("pbf:6", 10.0, 1000, 2, 216), ("apbf:dtc", 7.5, 800, 2, 216), ("apbf:dtvs", 8.25, 900, 2, 216)],
+        [("apbf", 3.0, 10, 1, 8)],
+        [("pbf:3", 2.0, 30, 1, 5), ("pbf:6", 4.0, 60, 1, 5), ("apbf", 0.0, 40, 1, 5)],
+    ]
+    tokens = ["pbf", "pbf:0", "pbf:x", "pbf:6x", "pbf: 7", "pbf:-2", "apbf:bogus", "zzz", "apbf",
+              "apbf:dtc", "apbf:dtvs", "pbf:99999999999", "", "apbf:"]
+    modes = {}
+    for t in tokens:
+        try:
+            modes[t] = list(O.ref_parse_bench_mode(t))
+        except ValueError as e:
+            modes[t] = str(e)
+    out["bench"] = np.array([json.dumps({"reports": [[list(r) for r in rep] for rep in reports],
+                                         "texts": [O.ref_format_bench_report(rep) for rep in reports],
+                                         "modes": modes})])
+    np.savez_compressed(os.path.join(OUT, "harness.npz"), **out)
+
+
 if __name__ == "__main__":
     solver_case("dam_pbf_dtc", "dam_break", 1728 / 216000, SolverMode.PBF, LodModel.DTC, (5, 5), 4)
     solver_case("dam_apbf_dtvs", "dam_break", 1728 / 216000, SolverMode.APBF, LodModel.DTVS, (5, 10), 4)
     solver_case("multi_apbf_dtc", "multi_dam_break", 0.03, SolverMode.APBF, LodModel.DTC, (4, 8), 3)
     component_case()
     scenario_case()
+    harness_case()
     print("golden fixtures written to", OUT)
