@@ -13,6 +13,7 @@
 // Link with paper_1608_04721_b200/libapbf_gpu.so.
 #pragma once
 
+#include <algorithm>
 #include <cstdint>
 #include <functional>
 #include <stdexcept>
@@ -20,6 +21,7 @@
 #include <variant>
 #include <vector>
 
+#include "apbf/depth_splat.hpp"
 #include "apbf/solver.hpp"
 #include "apbf_gpu.h"
 
@@ -114,26 +116,38 @@ public:
     FrameStats stepFrame(ParticleSet<Scalar>& state, const Camera<Scalar>& cam,
                          const LodModelConfig<Scalar>& lodCfg, int frameIndex) {
         upload(state);
-        apbf_camera c{};
-        for (int a = 0; a < 3; ++a) {
-            c.eye[a] = float(cam.eye[a]);
-            c.look_at[a] = float(cam.lookAt[a]);
-            c.up[a] = float(cam.up[a]);
-        }
-        c.vertical_fov = float(cam.verticalFov);
-        c.width = cam.width;
-        c.height = cam.height;
-        c.near_clip = float(cam.nearClip);
-        apbf_lod_config l{};
-        l.model = lodCfg.model == LodModel::Dtc ? APBF_LOD_DTC : APBF_LOD_DTVS;
-        l.d_min = float(lodCfg.dMin);
-        l.d_max = float(lodCfg.dMax);
-        l.n_min = lodCfg.range.nMin;
-        l.n_max = lodCfg.range.nMax;
-        l.auto_range = lodCfg.autoRange;
+        const apbf_camera c = toC(cam);
+        const apbf_lod_config l = toC(lodCfg);
         return run(state, [&](apbf_frame_stats* st, apbf_error* e) {
             return apbf_gpu_step_frame(h_, &c, &l, frameIndex, st, e);
         });
+    }
+
+    // ---- device-resident use (the harness drop-in, apbf_gpu/runner.hpp) ----
+    // setState uploads once; stepFrameResident steps the resident state with
+    // stepFrame's semantics; getState downloads it (storage order).
+    void setState(const ParticleSet<Scalar>& state) { upload(state); }
+    void getState(ParticleSet<Scalar>& state) { download(state); }
+    FrameStats stepFrameResident(const Camera<Scalar>& cam, const LodModelConfig<Scalar>& lodCfg,
+                                 int frameIndex) {
+        const apbf_camera c = toC(cam);
+        const apbf_lod_config l = toC(lodCfg);
+        std::vector<double> res(size_t(cfg_.substeps) * size_t(cfg_.range.nMax) + 1);
+        apbf_frame_stats st{};
+        st.residuals = res.data();
+        st.residuals_capacity = int32_t(res.size());
+        apbf_error e{};
+        throwIfError(apbf_gpu_step_frame(h_, &c, &l, frameIndex, &st, &e), e);
+        return toStats(st, res);
+    }
+    // renderLevelImage (depth_splat.hpp:314-350) of the resident state, on
+    // the device (float32 positions, like the solver's).
+    ImageRgb renderLevelImage(const Camera<Scalar>& cam, Scalar r, const IterationRange& range) {
+        const apbf_camera c = toC(cam);
+        ImageRgb img(cam.width, cam.height);
+        apbf_error e{};
+        throwIfError(apbf_gpu_render_levels(h_, &c, float(r), range.nMin, range.nMax, img.rgb.data(), &e), e);
+        return img;
     }
 
     FrameStats stepFrameWithLevels(ParticleSet<Scalar>& state, int frameIndex) {
@@ -149,6 +163,43 @@ public:
     }
 
 private:
+    static apbf_camera toC(const Camera<Scalar>& cam) {
+        apbf_camera c{};
+        for (int a = 0; a < 3; ++a) {
+            c.eye[a] = float(cam.eye[a]);
+            c.look_at[a] = float(cam.lookAt[a]);
+            c.up[a] = float(cam.up[a]);
+        }
+        c.vertical_fov = float(cam.verticalFov);
+        c.width = cam.width;
+        c.height = cam.height;
+        c.near_clip = float(cam.nearClip);
+        return c;
+    }
+    static apbf_lod_config toC(const LodModelConfig<Scalar>& lodCfg) {
+        apbf_lod_config l{};
+        l.model = lodCfg.model == LodModel::Dtc ? APBF_LOD_DTC : APBF_LOD_DTVS;
+        l.d_min = float(lodCfg.dMin);
+        l.d_max = float(lodCfg.dMax);
+        l.n_min = lodCfg.range.nMin;
+        l.n_max = lodCfg.range.nMax;
+        l.auto_range = lodCfg.autoRange;
+        return l;
+    }
+    static FrameStats toStats(const apbf_frame_stats& st, const std::vector<double>& res) {
+        FrameStats out;
+        out.frame = st.frame;
+        out.wallMs = st.wall_ms;
+        out.avgDensityPct = st.avg_density_pct;
+        out.minDensityPct = st.min_density_pct;
+        out.maxDensityPct = st.max_density_pct;
+        out.totalIterations = st.total_iterations;
+        out.contacts = st.contacts;
+        out.residuals.assign(res.begin(),
+                             res.begin() + std::min<int32_t>(st.n_residuals, int32_t(res.size())));
+        return out;
+    }
+
     static void trampoline(void* user, int32_t substep, int32_t iter) {
         auto* self = static_cast<Solver*>(user);
         self->download(*self->observed_);
@@ -167,16 +218,7 @@ private:
         const int32_t rc = step(&st, &e);
         download(state);
         throwIfError(rc, e);
-        FrameStats out;
-        out.frame = st.frame;
-        out.wallMs = st.wall_ms;
-        out.avgDensityPct = st.avg_density_pct;
-        out.minDensityPct = st.min_density_pct;
-        out.maxDensityPct = st.max_density_pct;
-        out.totalIterations = st.total_iterations;
-        out.contacts = st.contacts;
-        out.residuals.assign(res.begin(), res.begin() + std::min<int32_t>(st.n_residuals, int32_t(res.size())));
-        return out;
+        return toStats(st, res);
     }
 
     void upload(const ParticleSet<Scalar>& s) {

@@ -24,3 +24,17 @@ def test_dropin_matches_reference_solver_bitwise(scenario, scale):
     out = subprocess.run([DEMO, scenario, scale, "4"], capture_output=True, text=True, timeout=600)
     assert out.returncode == 0, out.stdout + out.stderr
     assert "DROPIN OK" in out.stdout
+
+
+RUNNER = os.path.join(ROOT, "oracle", "_ref", "runner_demo")
+
+
+@pytest.mark.gpu
+@pytest.mark.skipif(not os.path.exists(RUNNER), reason="oracle/_ref/runner_demo not built")
+def test_runner_dropin_against_reference_harness():
+    """include/apbf_gpu/runner.hpp: the reference harness test expectations
+    for the GPU runScenario/runBench, and the reference's compareRuns
+    accepting the GPU metrics.csv against the reference's own double run."""
+    out = subprocess.run([RUNNER, str(8000 / 216000), "10"], capture_output=True, text=True, timeout=900)
+    assert out.returncode == 0, out.stdout + out.stderr
+    assert "RUNNER OK" in out.stdout
