@@ -169,6 +169,15 @@ int32_t apbf_gpu_step_frame(apbf_gpu_solver* s, const apbf_camera* cam, const ap
 int32_t apbf_gpu_step_frame_with_levels(apbf_gpu_solver* s, int32_t frame_index,
                                         apbf_frame_stats* out, apbf_error* err);
 
+/* Multi-camera stepFrame (the paper's multi-camera remark): per camera i
+ * the levels assignLevels would give (lod config i with the solver's range,
+ * solver.hpp:247-258), blended with blendLod (lod.hpp:160-172, elementwise
+ * max), then stepFrameWithLevels (:236-244) -- all on the device.  k >= 1.
+ * Single rank only. */
+int32_t apbf_gpu_step_frame_multi(apbf_gpu_solver* s, int32_t k, const apbf_camera* cams,
+                                  const apbf_lod_config* lods, int32_t frame_index, apbf_frame_stats* out,
+                                  apbf_error* err);
+
 /* Solver::iterationObserver (solver.hpp:222-224, called at :344).  The
  * callback runs on the host after each iteration; it may call
  * apbf_gpu_get_state on the same handle.  NULL removes it. */
@@ -277,6 +286,10 @@ int32_t apbf_gpu_lod_dtc(int32_t n, const float* positions, const apbf_camera* c
 int32_t apbf_gpu_lod_dtvs(int32_t n, const float* positions, const apbf_camera* cam,
                           const apbf_lod_config* lod, float radius, int32_t* levels_out,
                           apbf_error* err);
+
+/* blendLod (lod.hpp:160-172): out = elementwise max of k >= 1 level arrays
+ * of length n (levels[i] points at array i). */
+int32_t apbf_gpu_blend_lod(int32_t k, int32_t n, const int32_t* const* levels, int32_t* out, apbf_error* err);
 
 /* splat (depth_splat.hpp:201-228): width*height depths, +inf where unwritten. */
 int32_t apbf_gpu_splat(int32_t n, const float* positions, float radius, const apbf_camera* cam,

@@ -453,6 +453,30 @@ class Solver:
         rc = self._lib.apbf_gpu_get_state(self._h, *state_pointers(state), C.byref(err))
         raise_for(rc, err)
 
+    def step_frame_multi_resident(self, cams, lods, frame_index: int) -> FrameStats:
+        """Multi-camera frame: levels = blendLod of each camera's assignLevels,
+        then stepFrameWithLevels (apbf_gpu_step_frame_multi)."""
+        if len(cams) != len(lods):
+            raise ValueError("one LOD config per camera")
+        k = len(cams)
+        cs = (capi.apbf_camera * max(k, 1))(*[c.to_c() for c in cams])
+        ls = (capi.apbf_lod_config * max(k, 1))(*[l.to_c() for l in lods])
+        st = capi.apbf_frame_stats()
+        st.residuals = self._res
+        st.residuals_capacity = len(self._res)
+        err = capi.apbf_error()
+        rc = self._lib.apbf_gpu_step_frame_multi(self._h, k, cs, ls, frame_index, C.byref(st), C.byref(err))
+        raise_for(rc, err)
+        return FrameStats.from_c(st, self._res)
+
+    def step_frame_multi(self, state: ParticleSet, cams, lods, frame_index: int) -> FrameStats:
+        """step_frame_multi_resident on the caller's state (uploaded, stepped,
+        downloaded like step_frame)."""
+        self.upload(state)
+        st = self.step_frame_multi_resident(cams, lods, frame_index)
+        self.download(state)
+        return st
+
     def render_levels(self, cam: Camera, r: float, rng: IterationRange) -> np.ndarray:
         """renderLevelImage of the resident state (x, level) on the device."""
         out = np.zeros(max(1, cam.width * cam.height * 3), np.uint8)
@@ -641,6 +665,22 @@ def splat(positions, r: float, cam: Camera) -> np.ndarray:
     rc = lib.apbf_gpu_splat(p.shape[0], _fp(p), r, C.byref(cam.to_c()), _fp(out), C.byref(err))
     raise_for(rc, err)
     return out.reshape(cam.height, cam.width)
+
+
+def blend_lod(per_camera) -> np.ndarray:
+    """blendLod (lod.hpp:160-172): elementwise max of level arrays."""
+    arrs = [np.ascontiguousarray(a, np.int32) for a in per_camera]
+    if not arrs:
+        raise ValueError("blend requires at least one level array")
+    n = arrs[0].shape[0]
+    if any(a.shape[0] != n for a in arrs):
+        raise ValueError("level array length mismatch")
+    out = np.zeros(n, np.int32)
+    ptrs = (C.POINTER(C.c_int32) * len(arrs))(*[_ip(a) for a in arrs])
+    err = capi.apbf_error()
+    rc = capi.lib().apbf_gpu_blend_lod(len(arrs), n, ptrs, _ip(out), C.byref(err))
+    raise_for(rc, err)
+    return out
 
 
 def render_level_image(positions, levels, r: float, cam: Camera, rng: IterationRange) -> np.ndarray:

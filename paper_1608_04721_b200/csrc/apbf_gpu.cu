@@ -293,6 +293,8 @@ void run_lod(Workspace& ws, const float4* X, int n, const apbf_camera& cam, cons
         ws.depth.ensure(px);
         KL(k_fill_int<<<blocks((long long)px, 256), 256, 0, st>>>(ws.depth.p, (int)px, 0x7f800000));
         KL(k_splat<<<blocks(n, 256), 256, 0, st>>>(n, X, radius, f, ws.depth.p));
+        // each LOD pass counts its own visible sample (several per frame with cameras)
+        CK(cudaMemsetAsync(&ws.ctl.p->sample_count, 0, sizeof(int), st));
         KL(k_dtvs_gap<<<blocks(n, 256), 256, 0, st>>>(n, X, radius, f, ws.depth.p, ws.dist.p, ws.keys.p,
                                                    ws.ctl.p));
     } else {
@@ -373,6 +375,7 @@ struct apbf_gpu_solver {
     DBuf<float> coef;  // per-list-entry spiky coefficient, lambda -> delta-p (32-bit lists)
     DBuf<unsigned short> nbr16;  // compact lists (APBF_C16, default)
     DBuf<int4> lbase;            // compact lists: 3 layer bases + count per order position
+    DBuf<int> lvTmp;             // multi-camera frames: one camera's levels before the blend
     // cell-tile solver (apbf_tiles.cuh)
     DBuf<TileInfo> tileInfo;
     DBuf<int2> tileRuns;
@@ -1711,6 +1714,64 @@ int32_t apbf_gpu_step_frame(apbf_gpu_solver* s, const apbf_camera* cam, const ap
     return guarded(err, [&] {
         s->frame(true, cam, lod, frame_index, out);
         s->levels_valid = true;
+    });
+}
+
+int32_t apbf_gpu_step_frame_multi(apbf_gpu_solver* s, int32_t k, const apbf_camera* cams,
+                                  const apbf_lod_config* lods, int32_t frame_index, apbf_frame_stats* out,
+                                  apbf_error* err) {
+    return guarded(err, [&] {
+        if (k < 1) fail(APBF_ERR_INVALID_ARGUMENT, "blend requires at least one level array");
+        if (s->transport) fail(APBF_ERR_INVALID_ARGUMENT, "multi-camera frames run on one rank");
+        CK(cudaSetDevice(s->ws.device));
+        const int n = s->n;
+        int* LV = s->set[s->cur].LV.p;
+        cudaStream_t st = s->ws.stream;
+        for (int c = 0; c < k; ++c) {  // assignLevels per camera, then blendLod
+            apbf_lod_config lc = lods[c];
+            lc.n_min = s->cfg.n_min;  // lc.range = cfg_.range (solver.hpp:254)
+            lc.n_max = s->cfg.n_max;
+            if (s->cfg.mode == APBF_MODE_APBF) {
+                validate_lod(lc);
+                if (n > 0 && lc.model == APBF_LOD_DTVS) {
+                    if (!(s->radius > 0.0f)) fail(APBF_ERR_INVALID_ARGUMENT, "splat radius must be positive");
+                    (void)make_frame(cams[c]);
+                }
+            }
+            if (n == 0) continue;
+            int* dst = LV;
+            if (c > 0) {
+                s->lvTmp.ensure((size_t)n);
+                dst = s->lvTmp.p;
+            }
+            if (s->cfg.mode == APBF_MODE_PBF)
+                KL(k_fill_int<<<blocks(n, 256), 256, 0, st>>>(dst, n, s->cfg.n_max));
+            else
+                run_lod(s->ws, s->set[s->cur].X.p, n, cams[c], lc, s->radius, dst);
+            if (c > 0) KL(k_max_int<<<blocks(n, 256), 256, 0, st>>>(n, LV, dst));
+        }
+        LAUNCH_CHECK();
+        s->frame(false, nullptr, nullptr, frame_index, out);
+        s->levels_valid = true;
+    });
+}
+
+int32_t apbf_gpu_blend_lod(int32_t k, int32_t n, const int32_t* const* levels, int32_t* out, apbf_error* err) {
+    return guarded(err, [&] {
+        if (k < 1) fail(APBF_ERR_INVALID_ARGUMENT, "blend requires at least one level array");
+        if (n == 0) return;
+        Workspace& ws = component_ws();
+        ws.tmpi.ensure((size_t)n * 2);
+        int* a = ws.tmpi.p;
+        int* b = ws.tmpi.p + n;
+        CK(cudaMemcpyAsync(a, levels[0], sizeof(int) * n, cudaMemcpyHostToDevice, ws.stream));
+        for (int c = 1; c < k; ++c) {
+            CK(cudaMemcpyAsync(b, levels[c], sizeof(int) * n, cudaMemcpyHostToDevice, ws.stream));
+            KL(k_max_int<<<blocks(n, 256), 256, 0, ws.stream>>>(n, a, b));
+        }
+        LAUNCH_CHECK();
+        CK(cudaMemcpyAsync(out, a, sizeof(int) * n, cudaMemcpyDeviceToHost, ws.stream));
+        CK(cudaStreamSynchronize(ws.stream));
     });
 }
 
