@@ -331,9 +331,10 @@ def run_ours(args, world, rank, local, pg):
         def e2e_step(m, frame):
             st = view(m)
             if world == 1:
-                solver.upload(st, frame_inputs_only=True)
-            else:
-                solver.upload_slice(st, n_global, frame_inputs_only=True)
+                # stepFrame(ParticleSet&) in one call (apbf_gpu_step_frame_host):
+                # upload the frame's inputs, step, write the reordered state back
+                return solver.step_frame(st, cam, lod, frame), m
+            solver.upload_slice(st, n_global, frame_inputs_only=True)
             stats = solver.step_frame_resident(cam, lod, frame)
             m2 = solver._lib.apbf_gpu_particle_count(solver._h)
             out = view(m2)
@@ -364,11 +365,12 @@ def run_ours(args, world, rank, local, pg):
         e2e = {"value": its2 / (ms2 / 1e3), "unit": UNIT,
                "h2d_bytes_per_step": int(h2d_all), "d2h_bytes_per_step": int(d2h_all),
                "ms_per_step": ms2 / args.steps,
-               "note": "per step: every rank uploads the frame's inputs from pinned host arrays "
-                       "(apbf_gpu_set_state / apbf_gpu_slab_set_state: x, v, mass, inv_mass; x*, lambda "
-                       "and level are overwritten by stepFrame before they are read), steps, and downloads "
-                       "the whole reordered ParticleSet (apbf_gpu_get_state, 13 words per particle) -- "
-                       "the reference's stepFrame(ParticleSet&) contract"}
+               "note": "per step, from pinned host arrays: the frame's inputs are uploaded (x, v, mass, "
+                       "inv_mass; x*, lambda and level are overwritten by stepFrame before they are read), "
+                       "the frame runs, and the whole reordered ParticleSet (13 words per particle) is "
+                       "written back -- the reference's stepFrame(ParticleSet&) contract; 1 GPU: one "
+                       "apbf_gpu_step_frame_host call (download overlapped with the metrics pass), "
+                       "N GPUs: apbf_gpu_slab_set_state + step + apbf_gpu_get_state per rank"}
 
     if rank != 0:
         return 0

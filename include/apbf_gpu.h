@@ -169,6 +169,16 @@ int32_t apbf_gpu_step_frame(apbf_gpu_solver* s, const apbf_camera* cam, const ap
 int32_t apbf_gpu_step_frame_with_levels(apbf_gpu_solver* s, int32_t frame_index,
                                         apbf_frame_stats* out, apbf_error* err);
 
+/* stepFrame(ParticleSet& state, ...) on host arrays in one call: uploads what
+ * the frame reads (x, v, mass, inv_mass), steps, and writes the whole
+ * reordered state back into the same seven arrays.  Equivalent to
+ * set_state + step_frame + get_state, with the download started as soon as
+ * the last substep is done, overlapping the end-of-frame metrics pass. */
+int32_t apbf_gpu_step_frame_host(apbf_gpu_solver* s, int32_t n, float* x, float* x_star, float* v,
+                                 float* mass, float* inv_mass, float* lambda, int32_t* level,
+                                 const apbf_camera* cam, const apbf_lod_config* lod, int32_t frame_index,
+                                 apbf_frame_stats* out, apbf_error* err);
+
 /* Multi-camera stepFrame (the paper's multi-camera remark): per camera i
  * the levels assignLevels would give (lod config i with the solver's range,
  * solver.hpp:247-258), blended with blendLod (lod.hpp:160-172, elementwise

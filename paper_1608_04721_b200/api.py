@@ -509,13 +509,21 @@ class Solver:
     # --- reference semantics (state in, state out) ---
     def step_frame(self, state: ParticleSet, cam: Camera, lod_cfg: LodModelConfig,
                    frame_index: int) -> FrameStats:
-        self.upload(state)
+        """stepFrame(ParticleSet&) (solver.hpp:228-233) on the caller's arrays:
+        one apbf_gpu_step_frame_host call uploads what the frame reads, steps,
+        and writes the reordered state back in place (pinned arrays copy at
+        full PCIe rate)."""
+        state._normalise()
         self._observer_state = state
-        try:
-            stats = self.step_frame_resident(cam, lod_cfg, frame_index)
-        finally:
-            self.download(state)
-        return stats
+        st = capi.apbf_frame_stats()
+        st.residuals = self._res
+        st.residuals_capacity = len(self._res)
+        err = capi.apbf_error()
+        rc = self._lib.apbf_gpu_step_frame_host(self._h, state.count(), *state_pointers(state),
+                                                C.byref(cam.to_c()), C.byref(lod_cfg.to_c()), frame_index,
+                                                C.byref(st), C.byref(err))
+        raise_for(rc, err)
+        return FrameStats.from_c(st, self._res)
 
     def step_frame_with_levels(self, state: ParticleSet, frame_index: int) -> FrameStats:
         state._normalise()

@@ -130,6 +130,9 @@ SIGNATURES = {
     "apbf_gpu_splat": (C.c_int32, [C.c_int32, _fp, C.c_float, C.POINTER(apbf_camera), _fp, _ep]),
     "apbf_gpu_count_contacts": (C.c_int32, [C.c_int32, _fp, C.POINTER(apbf_sdf_primitive),
                                             C.c_int32, C.c_float, C.c_float, _lp, _ep]),
+    "apbf_gpu_step_frame_host": (C.c_int32, [C.c_void_p, C.c_int32, _fp, _fp, _fp, _fp, _fp, _fp, _ip,
+                                             C.POINTER(apbf_camera), C.POINTER(apbf_lod_config), C.c_int32,
+                                             C.POINTER(apbf_frame_stats), _ep]),
     "apbf_gpu_blend_lod": (C.c_int32, [C.c_int32, C.c_int32, C.POINTER(_ip), _ip, _ep]),
     "apbf_gpu_step_frame_multi": (C.c_int32, [C.c_void_p, C.c_int32, C.POINTER(apbf_camera),
                                               C.POINTER(apbf_lod_config), C.c_int32,

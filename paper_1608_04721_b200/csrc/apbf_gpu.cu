@@ -90,6 +90,10 @@ inline int blocks(long long n, int t) { return (int)std::max<long long>(1, (n + 
 
 // ------------------------------------------------------------- buffers
 
+// Bumped by every device (re)allocation: a captured frame graph holds raw
+// pointers, so it is re-recorded only when this changes.
+static unsigned long long g_alloc_gen = 0;
+
 template <class T>
 struct DBuf {
     T* p = nullptr;
@@ -108,6 +112,7 @@ struct DBuf {
         release();
         CK(cudaMalloc(&p, sizeof(T) * std::max<size_t>(m, 1)));
         n = std::max<size_t>(m, 1);
+        ++g_alloc_gen;
     }
 };
 
@@ -462,11 +467,18 @@ struct apbf_gpu_solver {
     ~apbf_gpu_solver() {
         drop_graph();
         for (auto& e : ev) cudaEventDestroy(e);
+        if (copy_stream) cudaStreamDestroy(copy_stream);
     }
 
     void allocate(int nn) {
-        drop_graph();
-        eager_seen = false;
+        const unsigned long long gen0 = g_alloc_gen;
+        allocate_buffers(nn);
+        if (g_alloc_gen != gen0) {  // new device pointers: the frame graph is stale
+            drop_graph();
+            eager_seen = false;
+        }
+    }
+    void allocate_buffers(int nn) {
         n = nn;
         const size_t m = (size_t)std::max(nn, 1);
         set[0].ensure(m);
@@ -892,12 +904,52 @@ struct apbf_gpu_solver {
 
     void run_frame(bool assign_lod, const apbf_camera* cam, const apbf_lod_config* lod) {
         enqueue_frame(assign_lod, cam, lod);
+        finish_frame();
+    }
+
+    // ---- stepFrame on host arrays with the download overlapped ----
+    // When host_out is set, the frame's result is packed and copied to the
+    // caller's arrays on copy_stream as soon as the last substep is done
+    // (event ev[5]), concurrently with the end-of-frame metrics pass.
+    struct HostOut {
+        float *x, *xs, *v, *mass, *inv_mass, *lambda;
+        int32_t* level;
+        bool queued;
+    };
+    HostOut* host_out = nullptr;
+    cudaStream_t copy_stream = nullptr;
+
+    void enqueue_download(cudaStream_t st, HostOut& o) {
+        const float4* dxs = (in_iteration && obs_xs) ? obs_xs : set[cur].XS.p;
+        float* d = stage.p;
+        KL(k_pack_state<<<blocks(n, 256), 256, 0, st>>>(n, set[cur].view(), dxs, d));
+        LAUNCH_CHECK();
+        const size_t n1 = sizeof(float) * (size_t)n, n3 = 3 * n1;
+        if (o.x) CK(cudaMemcpyAsync(o.x, d, n3, cudaMemcpyDeviceToHost, st));
+        if (o.xs) CK(cudaMemcpyAsync(o.xs, d + 3LL * n, n3, cudaMemcpyDeviceToHost, st));
+        if (o.v) CK(cudaMemcpyAsync(o.v, d + 6LL * n, n3, cudaMemcpyDeviceToHost, st));
+        if (o.mass) CK(cudaMemcpyAsync(o.mass, d + 9LL * n, n1, cudaMemcpyDeviceToHost, st));
+        if (o.inv_mass) CK(cudaMemcpyAsync(o.inv_mass, d + 10LL * n, n1, cudaMemcpyDeviceToHost, st));
+        if (o.lambda) CK(cudaMemcpyAsync(o.lambda, d + 11LL * n, n1, cudaMemcpyDeviceToHost, st));
+        if (o.level) CK(cudaMemcpyAsync(o.level, d + 12LL * n, n1, cudaMemcpyDeviceToHost, st));
+    }
+
+    // Wait for the enqueued frame (and its overlapped download, if any).
+    void finish_frame() {
+        if (host_out && n > 0) {
+            if (!copy_stream) CK(cudaStreamCreateWithFlags(&copy_stream, cudaStreamNonBlocking));
+            CK(cudaStreamWaitEvent(copy_stream, ev[5], 0));
+            enqueue_download(copy_stream, *host_out);
+            host_out->queued = true;
+        }
         CK(cudaStreamSynchronize(ws.stream));
+        if (host_out && n > 0) CK(cudaStreamSynchronize(copy_stream));
     }
 
     // ---- CUDA Graph of the whole frame (LOD + substeps + metrics) ----
     struct GraphKey {
-        int start, assign_lod, metrics, ktime, ptime, n, flags;
+        int start, assign_lod, metrics, ktime, ptime, n, flags, stride;
+        unsigned w0bits;
         long long caps[3];
         apbf_camera cam;
         apbf_lod_config lod;
@@ -922,6 +974,8 @@ struct apbf_gpu_solver {
                   (uniform_w ? 0x100000 : 0) | (chunk << 4) |
                   (block_threads << 8);
         k.caps[0] = nbrCap;
+        k.stride = list_stride;
+        std::memcpy(&k.w0bits, &w0, sizeof w0);
         k.caps[1] = listCap16;
         k.caps[2] = fbCap;
         if (assign_lod && cam) k.cam = *cam;
@@ -946,7 +1000,7 @@ struct apbf_gpu_solver {
             g_launches += graph_kernels;
             cur = key.start ^ (cfg.substeps & 1);
             kt_used = kt_used_graph;
-            CK(cudaStreamSynchronize(st));
+            finish_frame();
             return;
         }
         if (graphable && eager_seen && std::memcmp(&key, &seen_key, sizeof key) == 0) {
@@ -975,7 +1029,7 @@ struct apbf_gpu_solver {
             CK(cudaGraphLaunch(gexec, st));
             g_launches += graph_kernels;
             cur = key.start ^ (cfg.substeps & 1);
-            CK(cudaStreamSynchronize(st));
+            finish_frame();
             return;
         }
         run_frame(assign_lod, cam, lod);
@@ -1702,6 +1756,32 @@ int32_t apbf_gpu_get_state(apbf_gpu_solver* s, float* x, float* xs, float* v, fl
         if (lambda) CK(cudaMemcpyAsync(lambda, d + 11LL * n, n1, cudaMemcpyDeviceToHost, st));
         if (level) CK(cudaMemcpyAsync(level, d + 12LL * n, n1, cudaMemcpyDeviceToHost, st));
         CK(cudaStreamSynchronize(st));
+    });
+}
+
+int32_t apbf_gpu_step_frame_host(apbf_gpu_solver* s, int32_t n, float* x, float* x_star, float* v, float* mass,
+                                 float* inv_mass, float* lambda, int32_t* level, const apbf_camera* cam,
+                                 const apbf_lod_config* lod, int32_t frame_index, apbf_frame_stats* out,
+                                 apbf_error* err) {
+    return guarded(err, [&] {
+        if (n < 0) fail(APBF_ERR_INVALID_ARGUMENT, "negative particle count");
+        if (n > 0 && (!x || !x_star || !v || !mass || !inv_mass || !lambda || !level))
+            fail(APBF_ERR_INVALID_ARGUMENT, "every ParticleSet array is required");
+        if (s->transport) fail(APBF_ERR_INVALID_ARGUMENT, "step_frame_host runs on one rank");
+        CK(cudaSetDevice(s->ws.device));
+        s->allocate(n);
+        s->cur = 0;
+        s->upload_state(n, x, nullptr, v, mass, inv_mass, nullptr, nullptr);  // what stepFrame reads
+        apbf_gpu_solver::HostOut o{x, x_star, v, mass, inv_mass, lambda, level, false};
+        s->host_out = &o;
+        try {
+            s->frame(true, cam, lod, frame_index, out);
+        } catch (...) {
+            s->host_out = nullptr;
+            throw;
+        }
+        s->host_out = nullptr;
+        s->levels_valid = true;
     });
 }
 
