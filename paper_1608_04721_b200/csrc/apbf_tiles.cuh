@@ -300,7 +300,7 @@ __global__ void __launch_bounds__(kTileP) k_lambda_tile(
     if (ctl->abort) return;
     const int t = blockIdx.x;
     if (tileMax[t] < iter) return;
-    extern __shared__ __align__(16) unsigned char s_raw[];
+    extern __shared__ __align__(128) unsigned char s_raw[];
     float4* s_p = reinterpret_cast<float4*>(s_raw);
     float* s_w = reinterpret_cast<float*>(s_raw + sizeof(float4) * kCandMax);
     __shared__ int2 s_runs[kMaxRuns];
@@ -399,7 +399,7 @@ __global__ void __launch_bounds__(kTileP) k_deltap_tile(
         if (i < n && LV[i] == iter - 1) Pn[i] = Pc[i];
         return;
     }
-    extern __shared__ __align__(16) unsigned char s_raw[];
+    extern __shared__ __align__(128) unsigned char s_raw[];
     float4* s_p = reinterpret_cast<float4*>(s_raw);  // (x*, lambda) per candidate
     __shared__ int2 s_runs[kMaxRuns];
     const TileInfo ti = info[t];
