@@ -78,6 +78,11 @@ typedef struct apbf_solver_config {
     int32_t inactive_lambda_zero;
     int32_t deterministic;    /* accepted for API parity; the GPU path is always deterministic */
     int32_t record_residuals;
+    /* Opt-in PBF velocity post-pass (Macklin & Mueller 2013, eqs. 15-17), absent
+     * from the reference: XSPH viscosity c and vorticity-confinement epsilon.
+     * 0 (the default) = off, and frames stay bit-identical to the reference. */
+    float xsph_viscosity;
+    float vorticity_epsilon;
 } apbf_solver_config;
 
 /* One SDF primitive (sdf.hpp:18-74).  Constructors' validation and the

@@ -104,6 +104,9 @@ class SolverConfig:
     inactive_lambda_zero: bool = False
     deterministic: bool = False
     record_residuals: bool = False
+    # opt-in PBF post-pass, absent from the reference (0 = off, bit-identical frames)
+    xsph_viscosity: float = 0.0
+    vorticity_epsilon: float = 0.0
 
     def dt_substep(self) -> float:
         return float(F32(self.dt_frame) / F32(self.substeps))
@@ -160,6 +163,8 @@ class SolverConfig:
         c.inactive_lambda_zero = int(self.inactive_lambda_zero)
         c.deterministic = int(self.deterministic)
         c.record_residuals = int(self.record_residuals)
+        c.xsph_viscosity = self.xsph_viscosity
+        c.vorticity_epsilon = self.vorticity_epsilon
         return c
 
 

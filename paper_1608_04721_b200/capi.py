@@ -37,7 +37,8 @@ class apbf_solver_config(C.Structure):
                 ("stab_iterations", C.c_int32), ("stab_threshold", C.c_int32),
                 ("particle_radius", C.c_float), ("mode", C.c_int32),
                 ("velocity_cap", C.c_float), ("inactive_lambda_zero", C.c_int32),
-                ("deterministic", C.c_int32), ("record_residuals", C.c_int32)]
+                ("deterministic", C.c_int32), ("record_residuals", C.c_int32),
+                ("xsph_viscosity", C.c_float), ("vorticity_epsilon", C.c_float)]
 
 
 class apbf_sdf_primitive(C.Structure):

@@ -14,6 +14,7 @@
 
 #include "apbf_tiles.cuh"
 #include "apbf_c16.cuh"
+#include "apbf_post.cuh"
 #include "apbf_dist.cuh"
 #include "apbf_transport.h"
 
@@ -378,7 +379,7 @@ struct apbf_gpu_solver {
     DBuf<int> order, nbrCount, nbr, tileCount, levelCount, activeCount, bucketStart;
     DBuf<long long> groupBase;
     DBuf<float> coef;  // per-list-entry spiky coefficient, lambda -> delta-p (32-bit lists)
-    DBuf<unsigned short> nbr16;  // compact lists (APBF_C16, default)
+    DBuf<unsigned short> nbr16;  // compact lists (APBF_C16=1)
     DBuf<int4> lbase;            // compact lists: 3 layer bases + count per order position
     DBuf<int> lvTmp;             // multi-camera frames: one camera's levels before the blend
     // cell-tile solver (apbf_tiles.cuh)
@@ -452,6 +453,10 @@ struct apbf_gpu_solver {
         if (const char* v = std::getenv("APBF_COEF_CACHE")) use_coef = std::atoi(v) != 0;
         if (const char* v = std::getenv("APBF_TILES")) use_tiles = std::atoi(v) != 0;
         if (const char* v = std::getenv("APBF_C16")) use_c16 = std::atoi(v) != 0;
+        if (post_pass()) {  // the post-pass walks the 32-bit per-particle lists
+            use_c16 = false;
+            use_tiles = false;
+        }
         if (const char* v = std::getenv("APBF_BLOCK")) block_threads = std::atoi(v);
         if (const char* v = std::getenv("APBF_CHUNK")) chunk = std::atoi(v);
         if (const char* v = std::getenv("APBF_GRAPHS")) use_graphs = std::atoi(v) != 0;
@@ -486,6 +491,10 @@ struct apbf_gpu_solver {
         backup.ensure(m);
         PB.ensure(m);
         PL.ensure(m);
+        if (post_pass()) {
+            postOm.ensure(m);
+            postV.ensure(m);
+        }
         order.ensure(m);
         const size_t groups = (m + 31) / 32 + 1;
         nbrCount.ensure(groups * 32);
@@ -557,11 +566,14 @@ struct apbf_gpu_solver {
     // frames only permute it); single-GPU only -- a slab rank cannot see its ghosts'
     bool uniform_w = false;
     float w0 = 0.0f;
-    bool use_c16 = false;
+    bool use_c16 = false;  // APBF_C16=1: compact 16-bit lists (slower here: the passes are latency-bound)
+    // opt-in PBF velocity post-pass (config xsph_viscosity / vorticity_epsilon)
+    bool post_pass() const { return cfg.xsph_viscosity != 0.0f || cfg.vorticity_epsilon != 0.0f; }
+    DBuf<float4> postOm, postV;
     // 32-bit lists: rows per lane of every warp slab (k_build_lists_direct);
     // grows on overflow, never shrinks
     int list_stride = 64;
-    long long list_groups = 0;  // APBF_C16=1: compact 16-bit lists (slower here: the passes are latency-bound)
+    long long list_groups = 0;
     int block_threads = 128;  // APBF_BLOCK: CTA size of the order-based passes
     int chunk = 4;            // APBF_CHUNK: neighbours gathered per batch (1, 2, 4, 8)
     int ownB_ = 0, ownE_ = 0x7fffffff;  // owned slot range (slab mode); everything otherwise
@@ -883,6 +895,15 @@ struct apbf_gpu_solver {
             float4* Pf = P[lastIter & 1];
             KL(k_finalize<<<blocks(n, 256), 256, 0, st>>>(n, ctl, Pf, dst.XS, dst.X, dst.V, dt, cap,
                                                        Pf != dst.XS ? 1 : 0, s));
+            if (post_pass()) {  // opt-in XSPH / vorticity confinement (apbf_post.cuh)
+                const KernelConsts kc = make_kernel_consts(cfg.h);
+                KL(k_post_omega<<<blocks(n, 256), 256, 0, st>>>(n, ctl, order.p, dst.X, dst.V, nbr.p,
+                                                             nbrCount.p, groupBase.p, kc,
+                                                             cfg.xsph_viscosity, postOm.p, postV.p));
+                KL(k_post_apply<<<blocks(n, 256), 256, 0, st>>>(n, ctl, order.p, dst.X, postOm.p, postV.p,
+                                                             nbr.p, nbrCount.p, groupBase.p, kc, dt,
+                                                             cfg.vorticity_epsilon, cap, dst.V));
+            }
             LAUNCH_CHECK();
             cur ^= 1;
             mark(4);
@@ -1041,6 +1062,7 @@ struct apbf_gpu_solver {
                apbf_frame_stats* out) {
         CK(cudaSetDevice(ws.device));
         if (transport) {
+            if (post_pass()) fail(APBF_ERR_INVALID_ARGUMENT, "the velocity post-pass runs on one rank");
             frame_dist(assign_lod, cam, lod, frame_index, out);
             return;
         }
