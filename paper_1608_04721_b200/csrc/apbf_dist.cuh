@@ -29,7 +29,13 @@ __global__ void k_layer_hist(int n, const float4* __restrict__ P, const int* __r
                              const Ctl* ctl, int g, float h, int* __restrict__ hist) {
     if (ctl->abort) return;
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < n) atomicAdd(&hist[layer_of(ctl->grid[g], h, P[i].z)], 1 + LV[i]);
+    // storage order is cell order, so a warp's particles share few layers:
+    // one atomic per distinct layer of the warp (match + reduce), not per particle
+    const int key = i < n ? layer_of(ctl->grid[g], h, P[i].z) : -1;
+    const int val = i < n ? 1 + LV[i] : 0;
+    const unsigned same = __match_any_sync(0xffffffffu, key);
+    const int sum = __reduce_add_sync(same, val);
+    if (key >= 0 && (threadIdx.x & 31) == __ffs(same) - 1) atomicAdd(&hist[key], sum);
 }
 
 // Destination bit mask: bit q set when cz in [lo[q] - halo, hi[q] + halo).
@@ -232,10 +238,16 @@ __global__ void __launch_bounds__(kTileThreads) k_level_tiles(int n, const Ctl* 
 
 // sum of levels over [b, e) (the owned particles' particle-iterations).
 __global__ void k_level_sum(int b, int e, const int* __restrict__ LV, Ctl* ctl) {
+    __shared__ int s_part[32];
     const int i = b + blockIdx.x * blockDim.x + threadIdx.x;
-    int v = i < e ? LV[i] : 0;
-    v = warp_sum_i(v);
-    if ((threadIdx.x & 31) == 0 && v) atomicAdd(&ctl->total_iterations, (unsigned long long)v);
+    int v = warp_sum_i(i < e ? LV[i] : 0);
+    if ((threadIdx.x & 31) == 0) s_part[threadIdx.x >> 5] = v;
+    __syncthreads();
+    if (threadIdx.x < 32) {  // one atomic per block
+        v = threadIdx.x < (blockDim.x >> 5) ? s_part[threadIdx.x] : 0;
+        v = warp_sum_i(v);
+        if (threadIdx.x == 0 && v) atomicAdd(&ctl->total_iterations, (unsigned long long)v);
+    }
 }
 
 // Metrics ghost records: (x, y, z, mass) + owned flag in the w of a second
@@ -309,14 +321,25 @@ __global__ void k_gather_int(int n, const int* __restrict__ perm, const int* __r
 // metrics-grid cz range of the owned particles (positions X) -> minmax[2]
 __global__ void k_layer_minmax(int n, const float4* __restrict__ X, const Ctl* ctl, int g, float h,
                                int* __restrict__ minmax) {
+    __shared__ int s_lo[32], s_hi[32];
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     int lo = 0x7fffffff, hi = (int)0x80000000;
     if (i < n) lo = hi = layer_of(ctl->grid[g], h, X[i].z);
     lo = warp_min_i(lo);
     hi = warp_max_i(hi);
     if ((threadIdx.x & 31) == 0) {
-        atomicMin(&minmax[0], lo);
-        atomicMax(&minmax[1], hi);
+        s_lo[threadIdx.x >> 5] = lo;
+        s_hi[threadIdx.x >> 5] = hi;
+    }
+    __syncthreads();
+    if (threadIdx.x < 32) {  // one atomic pair per block
+        const bool in = threadIdx.x < (blockDim.x >> 5);
+        lo = warp_min_i(in ? s_lo[threadIdx.x] : 0x7fffffff);
+        hi = warp_max_i(in ? s_hi[threadIdx.x] : (int)0x80000000);
+        if (threadIdx.x == 0) {
+            atomicMin(&minmax[0], lo);
+            atomicMax(&minmax[1], hi);
+        }
     }
 }
 

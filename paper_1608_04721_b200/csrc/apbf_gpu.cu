@@ -1297,7 +1297,8 @@ struct apbf_gpu_solver {
     bool any_abort(Transport& T) {
         T.allreduce(&ws.ctl.p->abort, 1, RType::I32, ROp::Max, ws.stream);
         int a = 0;
-        CK(cudaMemcpy(&a, &ws.ctl.p->abort, sizeof(int), cudaMemcpyDeviceToHost));
+        CK(cudaMemcpyAsync(&a, &ws.ctl.p->abort, sizeof(int), cudaMemcpyDeviceToHost, ws.stream));
+        CK(cudaStreamSynchronize(ws.stream));
         return a != 0;
     }
 
@@ -1389,7 +1390,8 @@ struct apbf_gpu_solver {
             KL(k_layer_hist<<<blocks(n, 256), 256, 0, st>>>(n, src.XS, src.LV, ctl, 0, cfg.h, layerHist.p));
             T.allreduce(layerHist.p, dz, RType::I32, ROp::Sum, st);
             std::vector<int> h32(dz);
-            CK(cudaMemcpy(h32.data(), layerHist.p, sizeof(int) * dz, cudaMemcpyDeviceToHost));
+            CK(cudaMemcpyAsync(h32.data(), layerHist.p, sizeof(int) * dz, cudaMemcpyDeviceToHost, st));
+            CK(cudaStreamSynchronize(st));
             std::vector<long long> hist(h32.begin(), h32.end());
             std::vector<int> zr(2 * G);
             if (!slab_partition(hist.data(), dz, G, 2, zr.data(), zr.data() + G)) {
@@ -1546,8 +1548,9 @@ struct apbf_gpu_solver {
         CK(cudaMemcpyAsync(zRange.p + G, hi.data(), sizeof(int) * G, cudaMemcpyHostToDevice, st));
         T.allreduce(zRange.p, G, RType::I32, ROp::Min, st);
         T.allreduce(zRange.p + G, G, RType::I32, ROp::Max, st);
-        CK(cudaMemcpy(lo.data(), zRange.p, sizeof(int) * G, cudaMemcpyDeviceToHost));
-        CK(cudaMemcpy(hi.data(), zRange.p + G, sizeof(int) * G, cudaMemcpyDeviceToHost));
+        CK(cudaMemcpyAsync(lo.data(), zRange.p, sizeof(int) * G, cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(hi.data(), zRange.p + G, sizeof(int) * G, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
         for (int q = 0; q < G; ++q) {
             if (q == g) {
                 lo[q] = -(1 << 29);
@@ -1654,9 +1657,10 @@ struct apbf_gpu_solver {
                 key = std::min(key, k);
             }
             long long* dkey = reinterpret_cast<long long*>(bounds.p);
-            CK(cudaMemcpy(dkey, &key, sizeof(key), cudaMemcpyHostToDevice));
+            CK(cudaMemcpyAsync(dkey, &key, sizeof(key), cudaMemcpyHostToDevice, ws.stream));
             T.allreduce(dkey, 1, RType::I64, ROp::Min, ws.stream);
-            CK(cudaMemcpy(&key, dkey, sizeof(key), cudaMemcpyDeviceToHost));
+            CK(cudaMemcpyAsync(&key, dkey, sizeof(key), cudaMemcpyDeviceToHost, ws.stream));
+            CK(cudaStreamSynchronize(ws.stream));
             if (key != NONE) {
                 static const char* names[kNumPassSlots] = {"predict", "prestabilize", "lambda",
                                                            "apply",   "finalize",     "finalize"};

@@ -32,10 +32,13 @@ struct Transport {
     virtual ~Transport() = default;
     virtual int rank() const = 0;
     virtual int size() const = 0;
-    // In-place all-reduce of a device buffer; returns with the result in place.
+    // In-place all-reduce of a device buffer, ordered on `st`: work enqueued on
+    // `st` afterwards sees the result; the host must synchronise `st` before
+    // reading it.
     virtual void allreduce(void* dev, size_t count, RType t, ROp op, cudaStream_t st) = 0;
-    // Device all-to-all: send[q] (sendBytes[q]) to rank q, recv[q] (recvBytes[q]) from
-    // rank q.  Entries for q == rank() are ignored (the caller copies locally).
+    // Device all-to-all, ordered on `st` like allreduce: send[q] (sendBytes[q])
+    // to rank q, recv[q] (recvBytes[q]) from rank q.  Entries for q == rank()
+    // are ignored (the caller copies locally).
     virtual void alltoallv(const void* const* send, const size_t* sendBytes, void* const* recv,
                            const size_t* recvBytes, cudaStream_t st) = 0;
     // Host all-to-all of one int64 per destination.
@@ -230,12 +233,15 @@ struct NcclTransport final : Transport {
     void check(int rc, const char* what) {
         if (rc != 0) throw std::runtime_error(std::string(what) + ": " + NcclApi::get().getErrorString(rc));
     }
+    // Both stream-ordered: no host synchronisation (NCCL runs on `st`).
     void allreduce(void* dev, size_t count, RType t, ROp op, cudaStream_t st) override {
         check(NcclApi::get().allReduce(dev, dev, count, nccl_type(t), nccl_op(op), comm, st), "ncclAllReduce");
-        if (cudaStreamSynchronize(st) != cudaSuccess) throw std::runtime_error("nccl allreduce sync");
     }
     void alltoallv(const void* const* send, const size_t* sendBytes, void* const* recv,
                    const size_t* recvBytes, cudaStream_t st) override {
+        bool any = false;
+        for (int q = 0; q < g_; ++q) any = any || (q != r_ && (sendBytes[q] || recvBytes[q]));
+        if (!any) return;  // nothing to exchange (e.g. one rank): no NCCL group
         NcclApi& api = NcclApi::get();
         check(api.groupStart(), "ncclGroupStart");
         for (int q = 0; q < g_; ++q) {
@@ -244,7 +250,6 @@ struct NcclTransport final : Transport {
             if (recvBytes[q]) check(api.recv(recv[q], recvBytes[q], 0, q, comm, st), "ncclRecv");
         }
         check(api.groupEnd(), "ncclGroupEnd");
-        if (cudaStreamSynchronize(st) != cudaSuccess) throw std::runtime_error("nccl alltoallv sync");
     }
     void alltoall_counts(const long long* send, long long* recv) override {
         // scratch layout: [0, g) send, [g, 2g) recv
