@@ -566,6 +566,27 @@ struct apbf_gpu_solver {
     // frames only permute it); single-GPU only -- a slab rank cannot see its ghosts'
     bool uniform_w = false;
     float w0 = 0.0f;
+    bool w_agreed = false;  // slab mode: uniform_w / w0 made global (agree_uniform_w)
+    DBuf<int> wflags;
+
+    // Slab mode: every rank uses the uniform-w lambda only if all ranks hold
+    // the same single inverse mass (ghosts come from other ranks).
+    void agree_uniform_w(Transport& T) {
+        if (w_agreed) return;
+        unsigned bits = 0;
+        std::memcpy(&bits, &w0, sizeof bits);
+        const bool any = n > 0;
+        int h[3] = {any && !uniform_w ? 0 : 1, any ? (int)bits : 0x7fffffff, any ? (int)bits : (int)0x80000000};
+        wflags.ensure(3);
+        CK(cudaMemcpyAsync(wflags.p, h, sizeof h, cudaMemcpyHostToDevice, ws.stream));
+        T.allreduce(wflags.p, 2, RType::I32, ROp::Min, ws.stream);
+        T.allreduce(wflags.p + 2, 1, RType::I32, ROp::Max, ws.stream);
+        CK(cudaMemcpyAsync(h, wflags.p, sizeof h, cudaMemcpyDeviceToHost, ws.stream));
+        CK(cudaStreamSynchronize(ws.stream));
+        uniform_w = h[0] == 1 && h[1] == h[2];
+        if (uniform_w) std::memcpy(&w0, &h[1], sizeof w0);
+        w_agreed = true;
+    }
     bool use_c16 = false;  // APBF_C16=1: compact 16-bit lists (slower here: the passes are latency-bound)
     // opt-in PBF velocity post-pass (config xsph_viscosity / vorticity_epsilon)
     bool post_pass() const { return cfg.xsph_viscosity != 0.0f || cfg.vorticity_epsilon != 0.0f; }
@@ -1243,7 +1264,8 @@ struct apbf_gpu_solver {
             levels_valid = bad == 0;
         }
         uniform_w = false;
-        if (!transport && inv_mass) {
+        w_agreed = false;  // slab ranks agree on uniformity at their next frame
+        if (inv_mass) {
             unsigned diff = 0;
             const unsigned* b = reinterpret_cast<const unsigned*>(inv_mass);
             for (int i = 1; i < nn; ++i) diff |= b[i] ^ b[0];
@@ -1616,6 +1638,7 @@ struct apbf_gpu_solver {
         std::vector<long long> cnt = all_counts(T, n);
         long long nAll = 0;
         for (long long c : cnt) nAll += c;
+        agree_uniform_w(T);
         if (assign_lod && cfg.mode == APBF_MODE_APBF) {
             apbf_lod_config lc = *lod;
             validate_lod(lc);

@@ -13,10 +13,14 @@ pytestmark = pytest.mark.gpu
 FIELDS = ("x", "x_star", "v", "mass", "inv_mass", "lambda_", "level")
 
 
-def compare(spec, G, frames, seed=1):
+def compare(spec, G, frames, seed=1, vary_mass_from=None):
     one = Solver(spec.solver, spec.scene)
     grp = SlabGroup(spec.solver, spec.scene, nranks=G, devices=[0] * G)
     a = S.make_state(spec, seed)
+    if vary_mass_from is not None:  # non-uniform inverse mass on the last slice only
+        k = vary_mass_from
+        a.mass[k:] = (a.mass[k:] * np.float32(1.5)).astype(np.float32)
+        a.inv_mass[k:] = (np.float32(1) / a.mass[k:]).astype(np.float32)
     b = a.copy()
     one.upload(a)
     grp.upload(b)
@@ -41,6 +45,13 @@ def test_slabs_bitwise_dam_break_apbf(G):
     spec.lod.range = spec.solver.range
     spec.lod.model = LodModel.DTVS
     compare(spec, G, 6)
+
+
+def test_slabs_bitwise_with_one_rank_holding_other_masses():
+    """Only the last rank's slice has a different mass: no rank may take the
+    uniform-inverse-mass lambda (the ranks agree on it at the first frame)."""
+    spec = S.build_scenario("dam_break", 8000 / 216000)
+    compare(spec, 2, 4, vary_mass_from=6000)
 
 
 def test_slabs_bitwise_pbf_dtc():
