@@ -845,6 +845,7 @@ struct apbf_gpu_solver {
             const int smemG = (nMax + 1) * (int)sizeof(int);
             KL(k_gather<<<numTiles, kTileThreads, smemG, st>>>(n, ctl, ws.perm.p, src, dst, nMax, numTiles,
                                                            tileCount.p));
+            if (s == cfg.substeps - 1) rec(ev[7]);  // final storage order (overlapped download)
             KL(k_level_scan<<<nMax + 1, 1024, 0, st>>>(ctl, numTiles, tileCount.p, levelCount.p));
             KL(k_level_finish<<<1, 32, 0, st>>>(ctl, n, nMax, levelCount.p, activeCount.p, bucketStart.p));
             if (use_tiles && !transport) {
@@ -961,26 +962,31 @@ struct apbf_gpu_solver {
     HostOut* host_out = nullptr;
     cudaStream_t copy_stream = nullptr;
 
+    // The frame's result to the caller's arrays on `st`: the fields that are
+    // final after the last substep's reorder once ev[7] has fired (during that
+    // substep's iterations), the rest once ev[5] has (during the metrics pass).
     void enqueue_download(cudaStream_t st, HostOut& o) {
-        const float4* dxs = (in_iteration && obs_xs) ? obs_xs : set[cur].XS.p;
+        const StateSet fin = set[cur].view();
         float* d = stage.p;
-        KL(k_pack_state<<<blocks(n, 256), 256, 0, st>>>(n, set[cur].view(), dxs, d));
-        LAUNCH_CHECK();
         const size_t n1 = sizeof(float) * (size_t)n, n3 = 3 * n1;
+        CK(cudaStreamWaitEvent(st, ev[7], 0));
+        KL(k_pack_static<<<blocks(n, 256), 256, 0, st>>>(n, fin, d));
+        if (o.mass) CK(cudaMemcpyAsync(o.mass, d + 9LL * n, n1, cudaMemcpyDeviceToHost, st));
+        if (o.inv_mass) CK(cudaMemcpyAsync(o.inv_mass, d + 10LL * n, n1, cudaMemcpyDeviceToHost, st));
+        if (o.level) CK(cudaMemcpyAsync(o.level, d + 12LL * n, n1, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamWaitEvent(st, ev[5], 0));
+        KL(k_pack_dynamic<<<blocks(n, 256), 256, 0, st>>>(n, fin, d));
+        LAUNCH_CHECK();
         if (o.x) CK(cudaMemcpyAsync(o.x, d, n3, cudaMemcpyDeviceToHost, st));
         if (o.xs) CK(cudaMemcpyAsync(o.xs, d + 3LL * n, n3, cudaMemcpyDeviceToHost, st));
         if (o.v) CK(cudaMemcpyAsync(o.v, d + 6LL * n, n3, cudaMemcpyDeviceToHost, st));
-        if (o.mass) CK(cudaMemcpyAsync(o.mass, d + 9LL * n, n1, cudaMemcpyDeviceToHost, st));
-        if (o.inv_mass) CK(cudaMemcpyAsync(o.inv_mass, d + 10LL * n, n1, cudaMemcpyDeviceToHost, st));
         if (o.lambda) CK(cudaMemcpyAsync(o.lambda, d + 11LL * n, n1, cudaMemcpyDeviceToHost, st));
-        if (o.level) CK(cudaMemcpyAsync(o.level, d + 12LL * n, n1, cudaMemcpyDeviceToHost, st));
     }
 
     // Wait for the enqueued frame (and its overlapped download, if any).
     void finish_frame() {
         if (host_out && n > 0) {
             if (!copy_stream) CK(cudaStreamCreateWithFlags(&copy_stream, cudaStreamNonBlocking));
-            CK(cudaStreamWaitEvent(copy_stream, ev[5], 0));
             enqueue_download(copy_stream, *host_out);
             host_out->queued = true;
         }
