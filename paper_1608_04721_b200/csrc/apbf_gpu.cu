@@ -1397,12 +1397,14 @@ struct apbf_gpu_solver {
             KL(k_list_reset<<<1, 1, 0, st>>>(ctl));
             KL(k_predict<<<blocks(n, 256), 256, 0, st>>>(n, src.X, src.V, src.XS, dt, cfg.gravity[0],
                                                       cfg.gravity[1], cfg.gravity[2], ctl, s));
-            if (any_abort(T)) break;
-            // global grid: AABB all-reduce (ordered ints), identical params everywhere
+            // global grid: AABB all-reduce (ordered ints), identical params
+            // everywhere; the abort flag travels with it (one host sync)
+            T.allreduce(&ctl->abort, 1, RType::I32, ROp::Max, st);
             T.allreduce(&ctl->grid[0].lo_ord[0], 3, RType::I32, ROp::Min, st);
             T.allreduce(&ctl->grid[0].hi_ord[0], 3, RType::I32, ROp::Max, st);
             KL(k_grid_params<<<1, 1, 0, st>>>(ctl, 0, cfg.h, cfg.h));
             ws.read_ctl();
+            if (ws.h_ctl->abort) break;
             if (std::getenv("APBF_DEBUG_SLAB")) {
                 const GridDev& gd = ws.h_ctl->grid[0];
                 std::fprintf(stderr, "[slab %d/%d] s=%d n=%d lo=(%g %g %g) hi=(%g %g %g) dims=(%d %d %d) cells=%lld rt=%d\n",
