@@ -1,3 +1,5 @@
+"""Four frames of the 1-rank NCCL slab path on ocean_1m (for an ncu launch list:
+`ncu --metrics gpu__time_duration.sum ... python tools/slab_only.py`)."""
 import os, sys
 sys.path.insert(0, os.getcwd())
 from paper_1608_04721_b200 import scenario as S
