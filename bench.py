@@ -121,16 +121,20 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
-def ncu_traffic(kernel: str):
-    """Per-launch DRAM bytes of `kernel` from the committed ncu --set full
-    summary (profiles/ncu_summary.json), or None."""
+def ncu_kernel(kernel: str):
+    """(DRAM bytes, duration in s) of one full-activity launch of `kernel` from
+    the committed ncu --set full summary (profiles/ncu_summary.json), or
+    (None, None)."""
     path = os.path.join(ROOT, "profiles", "ncu_summary.json")
     try:
         with open(path) as f:
-            d = json.load(f)
-        return d["kernels"][kernel]["dram_bytes_per_launch"]
+            k = json.load(f)["kernels"][kernel]
+        v, unit = k["gpu__time_duration.sum"].split()
+        secs = float(v) * {"ns": 1e-9, "nsecond": 1e-9, "us": 1e-6, "usecond": 1e-6, "ms": 1e-3,
+                           "msecond": 1e-3}[unit]
+        return k["dram_bytes_per_launch"], secs
     except Exception:
-        return None
+        return None, None
 
 
 def cpu_reference_sample(spec, seed, frames):
@@ -405,20 +409,26 @@ def run_ours(args, world, rank, local, pg):
         achieved = alg_bytes / (per_launch_ms / 1e3) / 1e9
         nbar = entries / n_global
         flops_pi = {"lambda": 37 * (nbar - 1) + 31, "deltap_apply": 23 * (nbar - 1) + 7}[dom]
+        traffic, t_ncu = ncu_kernel(f"k_{dom}")
+        traffic_gbs = traffic / t_ncu / 1e9 if traffic and t_ncu else None  # measured DRAM bytes / s
         sm_mhz = clk.get("sm_mhz") or 1965.0
         fp32_peak = 148 * 128 * sm_mhz * 1e6 / 1e12
         fp32_achieved = flops_pi * pis_per_launch / (per_launch_ms / 1e3) / 1e12
         line["roofline"] = {"bound": "hbm", "kernel": f"k_{dom}", "achieved": achieved,
                             "peak": hbm_peak, "unit": "GB/s", "frac": achieved / hbm_peak,
-                            "peak_source": peak_kind, "traffic": ncu_traffic(f"k_{dom}"),
+                            "peak_source": peak_kind, "traffic": traffic,
+                            "traffic_gbs_ncu": traffic_gbs,
+                            "traffic_frac_ncu": traffic_gbs / hbm_peak if traffic_gbs else None,
                             "algorithmic_bytes_per_launch": alg_bytes,
                             "avg_launch_ms": per_launch_ms, "launches": kt["launches"],
                             "share_of_step": dom_ms / ms_kt,
                             "share_of_step_both_passes": (kt["lambda_ms"] + kt["deltap_ms"]) / ms_kt,
                             "timing": f"CUDA events around every solver-pass launch on the solver stream, "
                                       f"over a twin region of the same {args.steps} frames",
-                            "note": "gather/latency-bound kernel; HBM fraction low by "
-                                    "construction (SURVEY.md 8d), see roofline_fp32"}
+                            "note": "gather/latency-bound kernel; the ALGORITHMIC-byte HBM fraction is low by "
+                                    "construction (SURVEY.md 8d: list/coefficient scratch excluded); "
+                                    "traffic_*_ncu = the measured DRAM bytes of one full launch over its "
+                                    "ncu duration; see also roofline_fp32"}
         line["roofline_fp32"] = {"bound": "fp32", "achieved": fp32_achieved, "peak": fp32_peak,
                                  "unit": "TFLOP/s", "frac": fp32_achieved / fp32_peak, "nbar": nbar,
                                  "flops_per_particle_iteration": flops_pi,
