@@ -1259,7 +1259,7 @@ struct apbf_gpu_solver {
     // so a caller that only steps frames need not upload them.  Without
     // levels, stepFrameWithLevels reports them out of range.
     void upload_state(int nn, const float* x, const float* xs, const float* v, const float* mass,
-                      const float* inv_mass, const float* lambda, const int32_t* level) {
+                      const float* inv_mass, const float* lambda, const int32_t* level, bool sync = true) {
         n = nn;
         levels_valid = level != nullptr || nn == 0;
         if (nn == 0) return;
@@ -1268,15 +1268,6 @@ struct apbf_gpu_solver {
             int bad = 0;
             for (int i = 0; i < nn; ++i) bad |= (level[i] < lo) | (level[i] > hi);
             levels_valid = bad == 0;
-        }
-        uniform_w = false;
-        w_agreed = false;  // slab ranks agree on uniformity at their next frame
-        if (inv_mass) {
-            unsigned diff = 0;
-            const unsigned* b = reinterpret_cast<const unsigned*>(inv_mass);
-            for (int i = 1; i < nn; ++i) diff |= b[i] ^ b[0];
-            uniform_w = diff == 0;
-            w0 = inv_mass[0];
         }
         cudaStream_t st = ws.stream;
         float* d = stage.p;
@@ -1288,10 +1279,20 @@ struct apbf_gpu_solver {
         CK(cudaMemcpyAsync(d + 10LL * nn, inv_mass, n1, cudaMemcpyHostToDevice, st));
         if (lambda) CK(cudaMemcpyAsync(d + 11LL * nn, lambda, n1, cudaMemcpyHostToDevice, st));
         if (level) CK(cudaMemcpyAsync(d + 12LL * nn, level, n1, cudaMemcpyHostToDevice, st));
+        // uniform inverse mass? (read on the host while the copies run)
+        uniform_w = false;
+        w_agreed = false;  // slab ranks agree on uniformity at their next frame
+        {
+            unsigned diff = 0;
+            const unsigned* b = reinterpret_cast<const unsigned*>(inv_mass);
+            for (int i = 1; i < nn; ++i) diff |= b[i] ^ b[0];
+            uniform_w = diff == 0;
+            w0 = inv_mass[0];
+        }
         const int have = (xs ? 1 : 0) | (lambda ? 2 : 0) | (level ? 4 : 0);
         KL(k_unpack_state<<<blocks(nn, 256), 256, 0, st>>>(nn, d, set[0].view(), have));
         LAUNCH_CHECK();
-        CK(cudaStreamSynchronize(st));
+        if (sync) CK(cudaStreamSynchronize(st));  // the caller may reuse its arrays on return
     }
 
     // Stable expansion of the `n` current particles by destination mask:
@@ -1828,7 +1829,9 @@ int32_t apbf_gpu_step_frame_host(apbf_gpu_solver* s, int32_t n, float* x, float*
         CK(cudaSetDevice(s->ws.device));
         s->allocate(n);
         s->cur = 0;
-        s->upload_state(n, x, nullptr, v, mass, inv_mass, nullptr, nullptr);  // what stepFrame reads
+        // what stepFrame reads; no sync: the frame follows on the same stream and
+        // the caller's arrays are untouched until this call returns
+        s->upload_state(n, x, nullptr, v, mass, inv_mass, nullptr, nullptr, false);
         apbf_gpu_solver::HostOut o{x, x_star, v, mass, inv_mass, lambda, level, false};
         s->host_out = &o;
         try {
@@ -2416,6 +2419,8 @@ int32_t apbf_gpu_slab_set_state(apbf_gpu_solver* s, int32_t n_local, int64_t n_g
                                 const float* lambda, const int32_t* level, apbf_error* err) {
     return guarded(err, [&] {
         if (!s->transport) fail(APBF_ERR_INVALID_ARGUMENT, "solver is not attached to a slab transport");
+        if (n_local > 0 && (!x || !v || !mass || !inv_mass))
+            fail(APBF_ERR_INVALID_ARGUMENT, "x, v, mass and inv_mass are required");
         CK(cudaSetDevice(s->ws.device));
         s->set_state_local(n_local, n_global, x, xs, v, mass, inv_mass, lambda, level);
     });
