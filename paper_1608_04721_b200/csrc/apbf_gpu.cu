@@ -449,6 +449,8 @@ struct apbf_gpu_solver {
         cap = cfg.velocity_cap > 0.0f ? cfg.velocity_cap : cfg.h / dt;
         S = cfg.stab_threshold > 0 ? cfg.stab_threshold : cfg.n_max;
         for (auto& e : ev) CK(cudaEventCreate(&e));
+        CK(cudaEventCreateWithFlags(&ev_x, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&ev_inputs, cudaEventDisableTiming));
         if (const char* v = std::getenv("APBF_STAGE_LISTS")) use_stage = std::atoi(v) != 0;
         if (const char* v = std::getenv("APBF_COEF_CACHE")) use_coef = std::atoi(v) != 0;
         if (const char* v = std::getenv("APBF_TILES")) use_tiles = std::atoi(v) != 0;
@@ -472,6 +474,8 @@ struct apbf_gpu_solver {
     ~apbf_gpu_solver() {
         drop_graph();
         for (auto& e : ev) cudaEventDestroy(e);
+        if (ev_x) cudaEventDestroy(ev_x);
+        if (ev_inputs) cudaEventDestroy(ev_inputs);
         if (copy_stream) cudaStreamDestroy(copy_stream);
     }
 
@@ -820,7 +824,6 @@ struct apbf_gpu_solver {
         const SolverConsts sc = consts();
         const int nMax = cfg.n_max;
         rec(ev[0]);
-        copy_set(backup, set[cur]);  // frame-start state for a list-overflow retry
         kt_used = 0;
         n_iter = n;
         KL(k_frame_begin<<<1, 1, 0, st>>>(ctl));
@@ -834,6 +837,13 @@ struct apbf_gpu_solver {
                 run_lod(ws, set[cur].X.p, n, *cam, lc, radius, set[cur].LV.p);
             }
         }
+        // a host stepFrame uploads everything but x on copy_stream while LOD
+        // runs (upload_split); a no-op wait when nothing was uploaded that way
+        if (capturing) CK(cudaStreamWaitEvent(st, ev_inputs, cudaEventWaitExternal));
+        else CK(cudaStreamWaitEvent(st, ev_inputs, 0));
+        // frame-start state for a list-overflow retry (levels included: a
+        // retry's LOD recomputes the same ones from the same x)
+        copy_set(backup, set[cur]);
         mark(1);
         for (int s = 0; s < cfg.substeps; ++s) {
             StateSet src = set[cur].view(), dst = set[cur ^ 1].view();
@@ -961,6 +971,37 @@ struct apbf_gpu_solver {
     };
     HostOut* host_out = nullptr;
     cudaStream_t copy_stream = nullptr;
+    cudaEvent_t ev_x = nullptr, ev_inputs = nullptr;  // upload_split: x unpacked / everything unpacked
+
+    // The inputs of a host stepFrame: x on the solver stream (the LOD pass
+    // needs only x), v, mass and inverse mass on copy_stream, unpacked there
+    // once x is; the frame waits for ev_inputs after its LOD pass.
+    void upload_split(int nn, const float* x, const float* v, const float* mass, const float* inv_mass) {
+        n = nn;
+        levels_valid = nn == 0;
+        if (nn == 0) return;
+        if (!copy_stream) CK(cudaStreamCreateWithFlags(&copy_stream, cudaStreamNonBlocking));
+        cudaStream_t st = ws.stream;
+        float* d = stage.p;
+        const size_t n1 = sizeof(float) * (size_t)nn, n3 = 3 * n1;
+        CK(cudaMemcpyAsync(d, x, n3, cudaMemcpyHostToDevice, st));
+        KL(k_unpack_x<<<blocks(nn, 256), 256, 0, st>>>(nn, d, set[0].X.p));
+        CK(cudaEventRecord(ev_x, st));
+        CK(cudaMemcpyAsync(d + 6LL * nn, v, n3, cudaMemcpyHostToDevice, copy_stream));
+        CK(cudaMemcpyAsync(d + 9LL * nn, mass, n1, cudaMemcpyHostToDevice, copy_stream));
+        CK(cudaMemcpyAsync(d + 10LL * nn, inv_mass, n1, cudaMemcpyHostToDevice, copy_stream));
+        CK(cudaStreamWaitEvent(copy_stream, ev_x, 0));
+        KL(k_unpack_rest<<<blocks(nn, 256), 256, 0, copy_stream>>>(nn, d, set[0].view()));
+        LAUNCH_CHECK();
+        CK(cudaEventRecord(ev_inputs, copy_stream));
+        uniform_w = false;  // (read on the host while the copies run)
+        w_agreed = false;
+        unsigned diff = 0;
+        const unsigned* b = reinterpret_cast<const unsigned*>(inv_mass);
+        for (int i = 1; i < nn; ++i) diff |= b[i] ^ b[0];
+        uniform_w = diff == 0;
+        w0 = inv_mass[0];
+    }
 
     // The frame's result to the caller's arrays on `st`: the fields that are
     // final after the last substep's reorder once ev[7] has fired (during that
@@ -1829,9 +1870,9 @@ int32_t apbf_gpu_step_frame_host(apbf_gpu_solver* s, int32_t n, float* x, float*
         CK(cudaSetDevice(s->ws.device));
         s->allocate(n);
         s->cur = 0;
-        // what stepFrame reads; no sync: the frame follows on the same stream and
-        // the caller's arrays are untouched until this call returns
-        s->upload_state(n, x, nullptr, v, mass, inv_mass, nullptr, nullptr, false);
+        // what stepFrame reads, x first (the caller's arrays stay untouched
+        // until this call returns, so no sync)
+        s->upload_split(n, x, v, mass, inv_mass);
         apbf_gpu_solver::HostOut o{x, x_star, v, mass, inv_mass, lambda, level, false};
         s->host_out = &o;
         try {
