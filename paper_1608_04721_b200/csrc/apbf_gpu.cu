@@ -999,8 +999,8 @@ struct apbf_gpu_solver {
         unsigned diff = 0;
         const unsigned* b = reinterpret_cast<const unsigned*>(inv_mass);
         for (int i = 1; i < nn; ++i) diff |= b[i] ^ b[0];
-        uniform_w = diff == 0;
         w0 = inv_mass[0];
+        uniform_w = diff == 0 && std::isfinite(w0);
     }
 
     // The frame's result to the caller's arrays on `st`: the fields that are
@@ -1327,8 +1327,8 @@ struct apbf_gpu_solver {
             unsigned diff = 0;
             const unsigned* b = reinterpret_cast<const unsigned*>(inv_mass);
             for (int i = 1; i < nn; ++i) diff |= b[i] ^ b[0];
-            uniform_w = diff == 0;
             w0 = inv_mass[0];
+            uniform_w = diff == 0 && std::isfinite(w0);
         }
         const int have = (xs ? 1 : 0) | (lambda ? 2 : 0) | (level ? 4 : 0);
         KL(k_unpack_state<<<blocks(nn, 256), 256, 0, st>>>(nn, d, set[0].view(), have));
