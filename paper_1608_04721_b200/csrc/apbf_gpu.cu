@@ -568,9 +568,23 @@ struct apbf_gpu_solver {
     bool use_stage = false, use_coef = true, use_tiles = false;
     // every particle has the same inverse mass w0 (bitwise; checked at upload,
     // frames only permute it); single-GPU only -- a slab rank cannot see its ghosts'
-    bool uniform_w = false;
+    // what the uploaded inverse masses allow k_lambda to assume (its kW): 0
+    // nothing, 1 all finite, 2 all equal to the finite w0 -- checked at
+    // upload, and frames only permute them
+    int w_mode = 0;
     float w0 = 0.0f;
-    bool w_agreed = false;  // slab mode: uniform_w / w0 made global (agree_uniform_w)
+    bool w_agreed = false;  // slab mode: w_mode / w0 made global (agree_uniform_w)
+
+    void scan_inv_mass(int nn, const float* inv_mass) {
+        unsigned diff = 0, nonfinite = 0;
+        const unsigned* b = reinterpret_cast<const unsigned*>(inv_mass);
+        for (int i = 0; i < nn; ++i) {  // branch-free so it vectorises
+            diff |= b[i] ^ b[0];
+            nonfinite |= (b[i] & 0x7f800000u) == 0x7f800000u;
+        }
+        w0 = inv_mass[0];
+        w_mode = nonfinite ? 0 : (diff == 0 ? 2 : 1);
+    }
     DBuf<int> wflags;
 
     // Slab mode: every rank uses the uniform-w lambda only if all ranks hold
@@ -580,15 +594,15 @@ struct apbf_gpu_solver {
         unsigned bits = 0;
         std::memcpy(&bits, &w0, sizeof bits);
         const bool any = n > 0;
-        int h[3] = {any && !uniform_w ? 0 : 1, any ? (int)bits : 0x7fffffff, any ? (int)bits : (int)0x80000000};
+        int h[3] = {any ? w_mode : 2, any ? (int)bits : 0x7fffffff, any ? (int)bits : (int)0x80000000};
         wflags.ensure(3);
         CK(cudaMemcpyAsync(wflags.p, h, sizeof h, cudaMemcpyHostToDevice, ws.stream));
         T.allreduce(wflags.p, 2, RType::I32, ROp::Min, ws.stream);
         T.allreduce(wflags.p + 2, 1, RType::I32, ROp::Max, ws.stream);
         CK(cudaMemcpyAsync(h, wflags.p, sizeof h, cudaMemcpyDeviceToHost, ws.stream));
         CK(cudaStreamSynchronize(ws.stream));
-        uniform_w = h[0] == 1 && h[1] == h[2];
-        if (uniform_w) std::memcpy(&w0, &h[1], sizeof w0);
+        w_mode = h[0] == 2 ? (h[1] == h[2] ? 2 : 1) : h[0];  // min over ranks; equal w0 for 2
+        if (w_mode == 2) std::memcpy(&w0, &h[1], sizeof w0);
         w_agreed = true;
     }
     bool use_c16 = false;  // APBF_C16=1: compact 16-bit lists (slower here: the passes are latency-bound)
@@ -611,10 +625,14 @@ struct apbf_gpu_solver {
         Ctl* ctl = ws.ctl.p;
         const int sb = blocks(n_iter, kBT);
         const int smem = kS ? kSolverSmem : 0;
-        // uniform inverse mass: specialised lambda only for the default variant
+        // inverse-mass specialisations (w_mode) only for the default variant
         if constexpr (!kS && kC && kK == 4) {
-            if (uniform_w)
-                KL(k_lambda<kS, kC, kBT, kK, kZ, true><<<sb, kBT, smem, st>>>(
+            if (w_mode == 2)
+                KL(k_lambda<kS, kC, kBT, kK, kZ, 2><<<sb, kBT, smem, st>>>(
+                    n_iter, it, ctl, activeCount.p, order.p, Pc, dst.W, dst.L, nbr.p, nbrCount.p,
+                    groupBase.p, coef.p, sc, s, ownB_, ownE_, PL.p));
+            else if (w_mode == 1)
+                KL(k_lambda<kS, kC, kBT, kK, kZ, 1><<<sb, kBT, smem, st>>>(
                     n_iter, it, ctl, activeCount.p, order.p, Pc, dst.W, dst.L, nbr.p, nbrCount.p,
                     groupBase.p, coef.p, sc, s, ownB_, ownE_, PL.p));
             else
@@ -994,13 +1012,8 @@ struct apbf_gpu_solver {
         KL(k_unpack_rest<<<blocks(nn, 256), 256, 0, copy_stream>>>(nn, d, set[0].view()));
         LAUNCH_CHECK();
         CK(cudaEventRecord(ev_inputs, copy_stream));
-        uniform_w = false;  // (read on the host while the copies run)
         w_agreed = false;
-        unsigned diff = 0;
-        const unsigned* b = reinterpret_cast<const unsigned*>(inv_mass);
-        for (int i = 1; i < nn; ++i) diff |= b[i] ^ b[0];
-        w0 = inv_mass[0];
-        uniform_w = diff == 0 && std::isfinite(w0);
+        scan_inv_mass(nn, inv_mass);  // on the host while the copies run
     }
 
     // The frame's result to the caller's arrays on `st`: the fields that are
@@ -1060,7 +1073,7 @@ struct apbf_gpu_solver {
         k.ptime = phase_timing;
         k.n = n;
         k.flags = (use_tiles ? 1 : 0) | (use_stage ? 2 : 0) | (use_coef ? 4 : 0) | (use_c16 ? 8 : 0) |
-                  (uniform_w ? 0x100000 : 0) | (chunk << 4) |
+                  (w_mode << 20) | (chunk << 4) |
                   (block_threads << 8);
         k.caps[0] = nbrCap;
         k.stride = list_stride;
@@ -1320,16 +1333,8 @@ struct apbf_gpu_solver {
         CK(cudaMemcpyAsync(d + 10LL * nn, inv_mass, n1, cudaMemcpyHostToDevice, st));
         if (lambda) CK(cudaMemcpyAsync(d + 11LL * nn, lambda, n1, cudaMemcpyHostToDevice, st));
         if (level) CK(cudaMemcpyAsync(d + 12LL * nn, level, n1, cudaMemcpyHostToDevice, st));
-        // uniform inverse mass? (read on the host while the copies run)
-        uniform_w = false;
-        w_agreed = false;  // slab ranks agree on uniformity at their next frame
-        {
-            unsigned diff = 0;
-            const unsigned* b = reinterpret_cast<const unsigned*>(inv_mass);
-            for (int i = 1; i < nn; ++i) diff |= b[i] ^ b[0];
-            w0 = inv_mass[0];
-            uniform_w = diff == 0 && std::isfinite(w0);
-        }
+        w_agreed = false;  // slab ranks agree on w_mode at their next frame
+        scan_inv_mass(nn, inv_mass);  // on the host while the copies run
         const int have = (xs ? 1 : 0) | (lambda ? 2 : 0) | (level ? 4 : 0);
         KL(k_unpack_state<<<blocks(nn, 256), 256, 0, st>>>(nn, d, set[0].view(), have));
         LAUNCH_CHECK();

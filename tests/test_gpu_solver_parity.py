@@ -86,3 +86,24 @@ def test_mass_distribution_bitwise(uniform):
         gpu.step_frame(a, spec.camera, spec.lod, f)
         orc.step_frame(b, spec.camera, spec.lod, f)
         assert_same_state(a, b, f"frame {f}")
+
+
+def test_infinite_inverse_mass_reports_like_the_oracle():
+    """A particle with w = inf takes the general lambda (self pair skipped):
+    GPU and oracle fail the same way, or both run on -- bit for bit."""
+    from paper_1608_04721_b200 import NumericalError
+    spec = S.build_scenario("dam_break", 1728 / 216000)
+    a = S.make_state(spec, 2)
+    a.inv_mass[100] = np.float32(np.inf)
+    b = a.copy()
+    gpu, orc = Solver(spec.solver, spec.scene), OracleSolver(spec.solver, spec.scene)
+    errs = []
+    for sv, st in ((gpu, a), (orc, b)):
+        try:
+            sv.step_frame(st, spec.camera, spec.lod, 0)
+            errs.append(None)
+        except NumericalError as e:
+            errs.append((e.pass_, e.particle))
+    assert errs[0] == errs[1]
+    if errs[0] is None:
+        assert_same_state(a, b, "frame 0")
