@@ -789,6 +789,10 @@ struct apbf_gpu_solver {
     // (Re)allocate the order-based list store at nbrCap entries: compact
     // 16-bit entries, or 32-bit entries plus the coefficient cache.
     void alloc_lists() {
+        // k_build_lists_direct addresses the store with 32-bit entry offsets
+        // (about 65M particles at the default stride)
+        if (!use_c16 && nbrCap > 0xffffffffLL)
+            fail(APBF_ERR_RUNTIME, "neighbour-list store exceeds 2^32 entries: too many particles for one GPU");
         nbr.release();
         coef.release();
         nbr16.release();
