@@ -505,7 +505,8 @@ struct apbf_gpu_solver {
         groupBase.ensure(groups);
         lbase.ensure(groups * 32);
         list_groups = (long long)groups;
-        const long long need = use_c16 ? (long long)m * 48 + 4096 : list_groups * list_stride * 32;
+        const long long need = (use_c16 || staged_lists) ? (long long)m * 48 + 4096
+                                                         : list_groups * list_stride * 32;
         if (nbrCap < need) {
             nbrCap = need;
             alloc_lists();
@@ -613,6 +614,10 @@ struct apbf_gpu_solver {
     // grows on overflow, never shrinks
     int list_stride = 64;
     long long list_groups = 0;
+    // lists longer than this make the uniform stride too wasteful: fall back
+    // to k_build_lists<false> (per-warp slabs from an atomic allocator)
+    static constexpr int kMaxListStride = 128;
+    bool staged_lists = false;
     int block_threads = 128;  // APBF_BLOCK: CTA size of the order-based passes
     int chunk = 4;            // APBF_CHUNK: neighbours gathered per batch (1, 2, 4, 8)
     int ownB_ = 0, ownE_ = 0x7fffffff;  // owned slot range (slab mode); everything otherwise
@@ -676,6 +681,10 @@ struct apbf_gpu_solver {
         cudaStream_t st = ws.stream;
         if (use_c16)
             KL(k_build_lists<true><<<blocks(nn, kListThreads), kListThreads, 0, st>>>(
+                nn, ws.ctl.p, order.p, dst.XS, ws.cellCount.p, cfg.h, cfg.h * cfg.h, nbr.p, nbrCount.p,
+                groupBase.p, nbrCap, nbr16.p, lbase.p));
+        else if (staged_lists)
+            KL(k_build_lists<false><<<blocks(nn, kListThreads), kListThreads, 0, st>>>(
                 nn, ws.ctl.p, order.p, dst.XS, ws.cellCount.p, cfg.h, cfg.h * cfg.h, nbr.p, nbrCount.p,
                 groupBase.p, nbrCap, nbr16.p, lbase.p));
         else
@@ -789,10 +798,6 @@ struct apbf_gpu_solver {
     // (Re)allocate the order-based list store at nbrCap entries: compact
     // 16-bit entries, or 32-bit entries plus the coefficient cache.
     void alloc_lists() {
-        // k_build_lists_direct addresses the store with 32-bit entry offsets
-        // (about 65M particles at the default stride)
-        if (!use_c16 && nbrCap > 0xffffffffLL)
-            fail(APBF_ERR_RUNTIME, "neighbour-list store exceeds 2^32 entries: too many particles for one GPU");
         nbr.release();
         coef.release();
         nbr16.release();
@@ -807,9 +812,20 @@ struct apbf_gpu_solver {
         const int why = ws.h_ctl->list_overflow;
         if (!use_tiles) {
             if (why & 2) use_c16 = false;
-            if ((why & 1) && use_c16) nbrCap = std::max<long long>(nbrCap * 2, (long long)(used * 3 / 2));
-            if ((why & 1) && !use_c16) list_stride = std::max(list_stride + 16, (int)used_fb + 8);
-            if (!use_c16) nbrCap = std::max(nbrCap, list_groups * list_stride * 32);
+            const bool packed = use_c16 || staged_lists;  // slabs sized per warp by an allocator
+            if ((why & 1) && packed) nbrCap = std::max<long long>(nbrCap * 2, (long long)(used * 3 / 2));
+            if ((why & 1) && !packed) {
+                const int want = std::max(list_stride + 16, (int)used_fb + 8);
+                if (want > kMaxListStride) {
+                    // a few very long lists: a uniform stride would cost n x max;
+                    // switch to per-warp slabs from the allocating builder
+                    staged_lists = true;
+                    nbrCap = std::max<long long>(nbrCap, (long long)(used * 3 / 2));
+                } else {
+                    list_stride = want;
+                }
+            }
+            if (!use_c16 && !staged_lists) nbrCap = std::max(nbrCap, list_groups * list_stride * 32);
             alloc_lists();
             return;
         }
@@ -1077,7 +1093,7 @@ struct apbf_gpu_solver {
         k.ptime = phase_timing;
         k.n = n;
         k.flags = (use_tiles ? 1 : 0) | (use_stage ? 2 : 0) | (use_coef ? 4 : 0) | (use_c16 ? 8 : 0) |
-                  (w_mode << 20) | (chunk << 4) |
+                  (w_mode << 20) | (staged_lists ? 0x400000 : 0) | (chunk << 4) |
                   (block_threads << 8);
         k.caps[0] = nbrCap;
         k.stride = list_stride;

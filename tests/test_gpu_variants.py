@@ -77,10 +77,11 @@ def test_compact_lists_fall_back_when_offsets_overflow(monkeypatch):
         assert np.array_equal(getattr(a, k), getattr(b, k)), k
 
 
-def test_dense_cluster_widens_list_stride():
+def test_dense_cluster_switches_to_allocated_list_slabs():
     """Spacing h/4 gives ~270 neighbours per particle, far past the initial
-    64-row slab stride: the build flags the overflow, the host widens the
-    stride and re-runs the frame, which must still match the oracle."""
+    64-row slab stride and the 128-row cap: the build flags the overflow, the
+    host switches to per-warp slabs from the allocating builder and re-runs
+    the frame, which must still match the oracle."""
     from oracle.oracle import OracleSolver
     h = 0.1
     side = 14
