@@ -430,7 +430,7 @@ static int32_t grid_build(grid_t* g, int n, const R* pos, R h, R pad, apbf_error
     for (int i = 0; i < n; ++i) g->perm[cursor[cellOf[i]]++] = i;
     free(cursor);
     free(cellOf);
-    g->points = (R*)malloc(sizeof(R) * 3 * (size_t)n);
+    g->points = (R*)malloc(sizeof(R) * 3 * (size_t)(n > 0 ? n : 0));
     for (int k = 0; k < n; ++k)
         for (int a = 0; a < 3; ++a) g->points[3 * k + a] = pos[3 * g->perm[k] + a];
     return APBF_OK;
@@ -865,7 +865,7 @@ static int32_t lod_validate(const apbf_lod_config* lod, apbf_error* err) {
 static int32_t lod_dtc(int n, const R* pos, const apbf_camera* cam, const apbf_lod_config* lod,
                        int32_t* levels, apbf_error* err) {
     int32_t rc = lod_validate(lod, err);
-    if (rc || n == 0) return rc;
+    if (rc || n <= 0) return rc;
     R* dist = (R*)malloc(sizeof(R) * (size_t)n);
     for (int i = 0; i < n; ++i) {
         const R d[3] = {pos[3 * i] - cam->eye[0], pos[3 * i + 1] - cam->eye[1],
@@ -913,7 +913,7 @@ static int32_t lod_dtvs(int n, const R* pos, const apbf_camera* cam, const apbf_
     R dMin = lod->d_min, dMax = lod->d_max;
     int spread = 1;
     if (lod->auto_range) {
-        R* sample = (R*)malloc(sizeof(R) * (size_t)n);
+        R* sample = (R*)malloc(sizeof(R) * (size_t)(n > 0 ? n : 0));
         size_t m = 0;
         for (int i = 0; i < n; ++i)
             if (visible[i]) sample[m++] = gap[i];
