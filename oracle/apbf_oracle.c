@@ -866,7 +866,7 @@ static int32_t lod_dtc(int n, const R* pos, const apbf_camera* cam, const apbf_l
                        int32_t* levels, apbf_error* err) {
     int32_t rc = lod_validate(lod, err);
     if (rc || n <= 0) return rc;
-    R* dist = (R*)malloc(sizeof(R) * (size_t)n);
+    R* dist = (R*)calloc((size_t)n, sizeof(R));
     for (int i = 0; i < n; ++i) {
         const R d[3] = {pos[3 * i] - cam->eye[0], pos[3 * i + 1] - cam->eye[1],
                         pos[3 * i + 2] - cam->eye[2]};
