@@ -1282,14 +1282,34 @@ struct apbf_gpu_solver {
     DBuf<unsigned> destMask;
     DBuf<Rec> sendRec, recvRec;
     DBuf<float4> sendPM, recvPM;
-    std::vector<long long> prefixPre, prefixPost;
-    bool slab_error = false;
+    // owned counts before / after each substep: the global index of an error
+    // (prefix over lower ranks) is computed from them only if a frame fails
+    std::vector<long long> localPre, localPost, prefixPre, prefixPost;
+    DBuf<long long> countsX;
 
-    static long long prefix_of(const std::vector<long long>& c, int g) {
-        long long p = 0;
-        for (int q = 0; q < g; ++q) p += c[q];
-        return p;
+    void exchange_prefixes(Transport& T) {
+        const int G = T.size(), g = T.rank(), S2 = 2 * cfg.substeps;
+        std::vector<long long> rows((size_t)G * S2, 0);
+        for (int s = 0; s < cfg.substeps; ++s) {
+            rows[(size_t)g * S2 + s] = localPre[s];
+            rows[(size_t)g * S2 + cfg.substeps + s] = localPost[s];
+        }
+        countsX.ensure(rows.size());
+        CK(cudaMemcpyAsync(countsX.p, rows.data(), sizeof(long long) * rows.size(), cudaMemcpyHostToDevice,
+                           ws.stream));
+        T.allreduce(countsX.p, rows.size(), RType::I64, ROp::Sum, ws.stream);
+        CK(cudaMemcpyAsync(rows.data(), countsX.p, sizeof(long long) * rows.size(), cudaMemcpyDeviceToHost,
+                           ws.stream));
+        CK(cudaStreamSynchronize(ws.stream));
+        prefixPre.assign(cfg.substeps, 0);
+        prefixPost.assign(cfg.substeps, 0);
+        for (int s = 0; s < cfg.substeps; ++s)
+            for (int q = 0; q < g; ++q) {
+                prefixPre[s] += rows[(size_t)q * S2 + s];
+                prefixPost[s] += rows[(size_t)q * S2 + cfg.substeps + s];
+            }
     }
+    bool slab_error = false;
 
     std::vector<long long> all_counts(Transport& T, long long mine) {
         std::vector<long long> snd(T.size(), mine), rcv(T.size());
@@ -1440,8 +1460,8 @@ struct apbf_gpu_solver {
         Ctl* ctl = ws.ctl.p;
         const SolverConsts sc = consts();
         const int nMax = cfg.n_max;
-        prefixPre.assign(cfg.substeps, 0);
-        prefixPost.assign(cfg.substeps, 0);
+        localPre.assign(cfg.substeps, 0);
+        localPost.assign(cfg.substeps, 0);
         slab_error = false;
         long long nAll = 0;
         for (long long c : cnt) nAll += c;
@@ -1458,7 +1478,7 @@ struct apbf_gpu_solver {
             }
         }
         for (int s = 0; s < cfg.substeps; ++s) {
-            prefixPre[s] = prefix_of(cnt, g);
+            localPre[s] = n;
             StateSet src = set[cur].view(), dst = set[cur ^ 1].view();
             KL(k_grid_reset<<<1, 1, 0, st>>>(ctl, 0));
             KL(k_list_reset<<<1, 1, 0, st>>>(ctl));
@@ -1607,8 +1627,7 @@ struct apbf_gpu_solver {
                 CK(cudaMemcpyAsync(src.LV, dst.LV + ownB, sizeof(int) * m, cudaMemcpyDeviceToDevice, st));
             }
             n = nOwn;
-            cnt = all_counts(T, n);
-            prefixPost[s] = prefix_of(cnt, g);
+            localPost[s] = n;
         }
         CK(cudaEventRecord(ev[5], st));
         const bool aborted = any_abort(T);
@@ -1741,10 +1760,12 @@ struct apbf_gpu_solver {
             const Ctl& c = *ws.h_ctl;
             if (c.runtime_error) fail(APBF_ERR_RUNTIME, "grid cell count exceeds limit; domain blew up");
             if (slab_error) fail(APBF_ERR_RUNTIME, "too few grid layers for the slab decomposition");
-            // global first error: (substep, iteration, pass, global index)
+            // global first error: (substep, iteration, pass, global index) -- only
+            // when the frame aborted (the abort flag is already all-reduced)
             const long long NONE = 0x7fffffffffffffffLL;
             long long key = NONE;
-            for (int sl = 0; sl < kNumPassSlots; ++sl) {
+            if (c.abort) exchange_prefixes(T);
+            for (int sl = 0; c.abort && sl < kNumPassSlots; ++sl) {
                 if (c.bad[sl] == 0x7fffffff) continue;
                 const int sub = std::max(0, c.bad_substep[sl]);
                 const int itr = (sl == kPassLambda || sl == kPassApply) ? std::max(0, c.bad_iter[sl])
@@ -1754,11 +1775,13 @@ struct apbf_gpu_solver {
                 const long long k = (seq << 32) | gidx;
                 key = std::min(key, k);
             }
-            long long* dkey = reinterpret_cast<long long*>(bounds.p);
-            CK(cudaMemcpyAsync(dkey, &key, sizeof(key), cudaMemcpyHostToDevice, ws.stream));
-            T.allreduce(dkey, 1, RType::I64, ROp::Min, ws.stream);
-            CK(cudaMemcpyAsync(&key, dkey, sizeof(key), cudaMemcpyDeviceToHost, ws.stream));
-            CK(cudaStreamSynchronize(ws.stream));
+            if (c.abort) {
+                long long* dkey = reinterpret_cast<long long*>(bounds.p);
+                CK(cudaMemcpyAsync(dkey, &key, sizeof(key), cudaMemcpyHostToDevice, ws.stream));
+                T.allreduce(dkey, 1, RType::I64, ROp::Min, ws.stream);
+                CK(cudaMemcpyAsync(&key, dkey, sizeof(key), cudaMemcpyDeviceToHost, ws.stream));
+                CK(cudaStreamSynchronize(ws.stream));
+            }
             if (key != NONE) {
                 static const char* names[kNumPassSlots] = {"predict", "prestabilize", "lambda",
                                                            "apply",   "finalize",     "finalize"};
