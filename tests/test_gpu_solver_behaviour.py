@@ -247,6 +247,30 @@ def test_full_size_1m_frame_bitwise():
     assert ((a.level >= 5) & (a.level <= 10)).all()
 
 
+def test_full_size_c2_three_frames_bitwise():
+    """BASELINE config C2 at full size: the 254,016-particle double dam break
+    (APBF {5..10}, DTVS), three frames, every field bit-identical to the
+    oracle; then 20 more resident frames stay finite and in range."""
+    spec = S.build_scenario("double_dam_break", 0.3716)
+    assert spec.particle_count() == 254016
+    gpu, orc = Solver(spec.solver, spec.scene), O.OracleSolver(spec.solver, spec.scene)
+    a = S.make_state(spec, 1)
+    b = a.copy()
+    for f in range(3):
+        sa = gpu.step_frame(a, spec.camera, spec.lod, f)
+        sb = orc.step_frame(b, spec.camera, spec.lod, f)
+        assert (sa.total_iterations, sa.contacts, sa.min_density_pct, sa.max_density_pct) == \
+            (sb.total_iterations, sb.contacts, sb.min_density_pct, sb.max_density_pct), f
+        for k in ("x", "x_star", "v", "mass", "inv_mass", "lambda_", "level"):
+            assert np.array_equal(getattr(a, k), getattr(b, k)), (f, k)
+    gpu.upload(a)
+    for f in range(3, 23):
+        gpu.step_frame_resident(spec.camera, spec.lod, f)
+    gpu.download(a)
+    assert np.isfinite(a.x).all() and np.isfinite(a.v).all()
+    assert ((a.level >= 5) & (a.level <= 10)).all()
+
+
 @pytest.mark.slow
 @pytest.mark.skipif(not O.ref_available(), reason="oracle/_ref not built")
 def test_tier_b_float_gpu_vs_reference_double():
