@@ -1492,13 +1492,6 @@ struct apbf_gpu_solver {
             KL(k_grid_params<<<1, 1, 0, st>>>(ctl, 0, cfg.h, cfg.h));
             ws.read_ctl();
             if (ws.h_ctl->abort) break;
-            if (std::getenv("APBF_DEBUG_SLAB")) {
-                const GridDev& gd = ws.h_ctl->grid[0];
-                std::fprintf(stderr, "[slab %d/%d] s=%d n=%d lo=(%g %g %g) hi=(%g %g %g) dims=(%d %d %d) cells=%lld rt=%d\n",
-                             g, G, s, n, ord2f(gd.lo_ord[0]), ord2f(gd.lo_ord[1]), ord2f(gd.lo_ord[2]),
-                             ord2f(gd.hi_ord[0]), ord2f(gd.hi_ord[1]), ord2f(gd.hi_ord[2]), gd.dims[0], gd.dims[1],
-                             gd.dims[2], gd.cells, ws.h_ctl->runtime_error);
-            }
             if (ws.h_ctl->runtime_error) break;
             // slabs: equal-work split (sum of 1 + level per layer) of the global histogram
             const int dz = ws.h_ctl->grid[0].dims[2];

@@ -189,9 +189,12 @@ struct NcclApi {
             api.getUniqueId = (int (*)(void*))dlsym(api.lib, "ncclGetUniqueId");
             api.commInitRankSym = dlsym(api.lib, "ncclCommInitRank");
             api.commDestroy = (int (*)(void*))dlsym(api.lib, "ncclCommDestroy");
-            api.allReduce = (int (*)(const void*, void*, size_t, int, int, void*, cudaStream_t))dlsym(api.lib, "ncclAllReduce");
-            api.send = (int (*)(const void*, size_t, int, int, void*, cudaStream_t))dlsym(api.lib, "ncclSend");
-            api.recv = (int (*)(void*, size_t, int, int, void*, cudaStream_t))dlsym(api.lib, "ncclRecv");
+            using AllReduceFn = int (*)(const void*, void*, size_t, int, int, void*, cudaStream_t);
+            using SendFn = int (*)(const void*, size_t, int, int, void*, cudaStream_t);
+            using RecvFn = int (*)(void*, size_t, int, int, void*, cudaStream_t);
+            api.allReduce = (AllReduceFn)dlsym(api.lib, "ncclAllReduce");
+            api.send = (SendFn)dlsym(api.lib, "ncclSend");
+            api.recv = (RecvFn)dlsym(api.lib, "ncclRecv");
             api.groupStart = (int (*)())dlsym(api.lib, "ncclGroupStart");
             api.groupEnd = (int (*)())dlsym(api.lib, "ncclGroupEnd");
             api.getErrorString = (const char* (*)(int))dlsym(api.lib, "ncclGetErrorString");
