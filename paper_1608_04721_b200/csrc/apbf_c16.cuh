@@ -14,19 +14,6 @@
 
 namespace apbf_gpu {
 
-// Spiky gradient coefficient of one pair via the exact fast sqrt/division
-// (range argument in k_lambda); +0 where gradientKernel returns Zero().
-// Sets slow when the pair is outside the validated range.
-__device__ __forceinline__ float spiky_coef_fast(const KernelConsts& kc, float r2, bool& slow) {
-    const float rn = sqrt_fast(r2);
-    slow |= !sqrt_fast_ok(r2) && r2 != 0.0f;
-    const bool zero = (r2 == 0.0f) || (rn >= kc.h);
-    const float a = kc.h - rn;
-    const float num = kc.spiky * a * a;
-    slow |= !zero && !(num <= -0x1p-60f);
-    return zero ? 0.0f : div_fast(num, rn);
-}
-
 // computeLambda over compact lists; also publishes PL (see k_lambda).
 // kCoef: also cache each pair's coefficient for delta-p (as k_lambda).
 template <int kBT, int kK, bool kZero, bool kCoef>

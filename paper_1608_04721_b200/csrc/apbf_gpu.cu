@@ -563,10 +563,12 @@ struct apbf_gpu_solver {
     }
 
     // Variant switches for A/B measurements: APBF_STAGE_LISTS=1 stages list
-    // slabs in shared memory (bulk async copy); APBF_COEF_CACHE=0 makes the
-    // delta-p pass recompute the spiky coefficients instead of reading the
-    // lambda pass's cache.  Every variant is bit-identical.
-    bool use_stage = false, use_coef = true, use_tiles = false;
+    // slabs in shared memory (bulk async copy); APBF_COEF_CACHE=1 has the
+    // lambda pass store every pair's spiky coefficient for delta-p instead of
+    // delta-p recomputing it with the exact fast sqrt/division (streaming 4 B
+    // per pair each way costs more than the ~20 instructions it saves).
+    // Every variant is bit-identical.
+    bool use_stage = false, use_coef = false, use_tiles = false;
     // every particle has the same inverse mass w0 (bitwise; checked at upload,
     // frames only permute it); single-GPU only -- a slab rank cannot see its ghosts'
     // what the uploaded inverse masses allow k_lambda to assume (its kW): 0
@@ -631,7 +633,7 @@ struct apbf_gpu_solver {
         const int sb = blocks(n_iter, kBT);
         const int smem = kS ? kSolverSmem : 0;
         // inverse-mass specialisations (w_mode) only for the default variant
-        if constexpr (!kS && kC && kK == 4) {
+        if constexpr (!kS && kK == 4) {
             if (w_mode == 2)
                 KL(k_lambda<kS, kC, kBT, kK, kZ, 2><<<sb, kBT, smem, st>>>(
                     n_iter, it, ctl, activeCount.p, order.p, Pc, dst.W, dst.L, nbr.p, nbrCount.p,
@@ -803,7 +805,7 @@ struct apbf_gpu_solver {
         nbr16.release();
         if (use_c16) nbr16.ensure((size_t)nbrCap);
         else nbr.ensure((size_t)nbrCap);
-        if (use_coef || !use_c16) coef.ensure((size_t)nbrCap);
+        if (use_coef) coef.ensure((size_t)nbrCap);  // only the cache variant reads it
     }
 
     // After an overflowed list build: leave the compact encoding when its

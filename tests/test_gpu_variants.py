@@ -1,8 +1,9 @@
 """Every solver-pass variant selectable by environment (A/B switches read at
 Solver creation) must give the default path's frames bit for bit: compact
-16-bit lists with and without the coefficient cache, shared-memory list
-staging, the cell-tile solver, gather batch sizes, CTA size, eager launches
-instead of CUDA Graph replay.  Also the compact lists' range fallback."""
+16-bit lists with and without the coefficient cache, the coefficient cache
+itself, shared-memory list staging, the cell-tile solver, gather batch sizes,
+CTA size, eager launches instead of CUDA Graph replay.  Also the compact
+lists' range fallback and the list stride fallback."""
 import numpy as np
 import pytest
 
@@ -14,8 +15,8 @@ pytestmark = pytest.mark.gpu
 FIELDS = ("x", "x_star", "v", "mass", "inv_mass", "lambda_", "level")
 VARIANTS = [
     {"APBF_C16": "1"},
-    {"APBF_C16": "1", "APBF_COEF_CACHE": "0"},
-    {"APBF_COEF_CACHE": "0"},
+    {"APBF_C16": "1", "APBF_COEF_CACHE": "1"},
+    {"APBF_COEF_CACHE": "1"},
     {"APBF_STAGE_LISTS": "1"},
     {"APBF_TILES": "1"},
     {"APBF_CHUNK": "1"},
