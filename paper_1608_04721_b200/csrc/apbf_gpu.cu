@@ -652,7 +652,9 @@ struct apbf_gpu_solver {
                                                                  coef.p, sc, s, ownB_, ownE_, PL.p));
         }
         if (tslot >= 0) rec(kt_ev[tslot][1]);
-        KL(k_deltap_apply<kZ, kS, kC, kBT, kK><<<sb, kBT, smem, st>>>(
+        // delta-p runs best in 256-thread CTAs, lambda in 128 (measured)
+        constexpr int kDB = (!kS && kBT == 128) ? 256 : kBT;
+        KL(k_deltap_apply<kZ, kS, kC, kDB, kK><<<blocks(n_iter, kDB), kDB, smem, st>>>(
             n_iter, it, ctl, activeCount.p, order.p, Pc, Pn, dst.W, dst.L, dst.LV, nbr.p, nbrCount.p,
             groupBase.p, coef.p, ws.scene.p, sc, s, ownB_, ownE_, PL.p));
     }
