@@ -282,19 +282,12 @@ __global__ void k_density_stats_owned(int n, Ctl* ctl, const float4* __restrict_
             hi[a] = imin_std(c + 1, G.dims[a] - 1);
             if (lo[a] > hi[a]) any = false;
         }
-        if (any) {
-            for (int cz = lo[2]; cz <= hi[2]; ++cz)
-                for (int cy = lo[1]; cy <= hi[1]; ++cy) {
-                    const long long rowBase = ((long long)cz * G.dims[1] + cy) * G.dims[0];
-                    const int b = cellStart[rowBase + lo[0]];
-                    const int e = cellStart[rowBase + hi[0] + 1];
-                    for (int j = b; j < e; ++j) {
-                        const float4 pj = S[j];
-                        const float r2 = sqn3(q.x - pj.x, q.y - pj.y, q.z - pj.z);
-                        if (r2 < kc.h2) rho += pj.w * poly6_r2(kc, r2);
-                    }
-                }
-        }
+        if (any)
+            scan_candidates_all(G, cellStart, S, lo, hi, q.x, q.y, q.z, kc.h2,
+                                [&](int, const float4& pj, float r2, bool m) {
+                                    const float t = pj.w * poly6_r2_in(kc, r2);
+                                    rho += m ? t : 0.0f;
+                                });
     }
     double s = valid ? (double)rho : 0.0;
     int mn = valid ? f2ord(rho) : 0x7fffffff;

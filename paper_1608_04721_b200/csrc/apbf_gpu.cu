@@ -111,7 +111,7 @@ struct DBuf {
     void ensure(size_t m) {
         if (m <= n && p) return;
         release();
-        CK(cudaMalloc(&p, sizeof(T) * std::max<size_t>(m, 1)));
+        CK(cudaMalloc(&p, sizeof(T) * std::max<size_t>(m, 1) + kBufSlack));
         n = std::max<size_t>(m, 1);
         ++g_alloc_gen;
     }
