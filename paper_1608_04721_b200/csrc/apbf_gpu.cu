@@ -449,8 +449,13 @@ struct apbf_gpu_solver {
         cap = cfg.velocity_cap > 0.0f ? cfg.velocity_cap : cfg.h / dt;
         S = cfg.stab_threshold > 0 ? cfg.stab_threshold : cfg.n_max;
         for (auto& e : ev) CK(cudaEventCreate(&e));
-        CK(cudaEventCreateWithFlags(&ev_x, cudaEventDisableTiming));
-        CK(cudaEventCreateWithFlags(&ev_inputs, cudaEventDisableTiming));
+        const unsigned evf = std::getenv("APBF_E2E_TRACE") ? cudaEventDefault : cudaEventDisableTiming;
+        CK(cudaEventCreateWithFlags(&ev_x, evf));
+        CK(cudaEventCreateWithFlags(&ev_inputs, evf));
+        CK(cudaEventCreateWithFlags(&ev_vm, evf));
+        CK(cudaEventCreateWithFlags(&ev_bk_fork, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&ev_bk_join, cudaEventDisableTiming));
+        CK(cudaStreamCreateWithFlags(&bk_stream, cudaStreamNonBlocking));
         if (const char* v = std::getenv("APBF_STAGE_LISTS")) use_stage = std::atoi(v) != 0;
         if (const char* v = std::getenv("APBF_COEF_CACHE")) use_coef = std::atoi(v) != 0;
         if (const char* v = std::getenv("APBF_TILES")) use_tiles = std::atoi(v) != 0;
@@ -475,6 +480,10 @@ struct apbf_gpu_solver {
         drop_graph();
         for (auto& e : ev) cudaEventDestroy(e);
         if (ev_x) cudaEventDestroy(ev_x);
+        if (ev_vm) cudaEventDestroy(ev_vm);
+        if (ev_bk_fork) cudaEventDestroy(ev_bk_fork);
+        if (ev_bk_join) cudaEventDestroy(ev_bk_join);
+        if (bk_stream) cudaStreamDestroy(bk_stream);
         if (ev_inputs) cudaEventDestroy(ev_inputs);
         if (copy_stream) cudaStreamDestroy(copy_stream);
     }
@@ -535,9 +544,9 @@ struct apbf_gpu_solver {
         ws.ensure_cells();
     }
 
-    void copy_set(SetBufs& dst, SetBufs& src) {
+    void copy_set(SetBufs& dst, SetBufs& src, cudaStream_t st = nullptr) {
         const size_t m = (size_t)n;
-        cudaStream_t st = ws.stream;
+        if (!st) st = ws.stream;
         CK(cudaMemcpyAsync(dst.X.p, src.X.p, sizeof(float4) * m, cudaMemcpyDeviceToDevice, st));
         CK(cudaMemcpyAsync(dst.V.p, src.V.p, sizeof(float4) * m, cudaMemcpyDeviceToDevice, st));
         CK(cudaMemcpyAsync(dst.XS.p, src.XS.p, sizeof(float4) * m, cudaMemcpyDeviceToDevice, st));
@@ -578,6 +587,9 @@ struct apbf_gpu_solver {
     float w0 = 0.0f;
     bool w_agreed = false;  // slab mode: w_mode / w0 made global (agree_uniform_w)
 
+    bool w_known = false;               // w_mode/w0 hold a scan of an earlier upload
+    const float* pending_scan = nullptr;  // upload_split's host inverse mass, scanned in finish_frame
+    bool w_mismatch = false;            // that scan disagreed with the mode the frame ran with
     void scan_inv_mass(int nn, const float* inv_mass) {
         unsigned diff = 0, nonfinite = 0;
         const unsigned* b = reinterpret_cast<const unsigned*>(inv_mass);
@@ -879,24 +891,44 @@ struct apbf_gpu_solver {
                 run_lod(ws, set[cur].X.p, n, *cam, lc, radius, set[cur].LV.p);
             }
         }
-        // a host stepFrame uploads everything but x on copy_stream while LOD
-        // runs (upload_split); a no-op wait when nothing was uploaded that way
-        if (capturing) CK(cudaStreamWaitEvent(st, ev_inputs, cudaEventWaitExternal));
-        else CK(cudaStreamWaitEvent(st, ev_inputs, 0));
-        // frame-start state for a list-overflow retry (levels included: a
-        // retry's LOD recomputes the same ones from the same x)
-        copy_set(backup, set[cur]);
         mark(1);
         for (int s = 0; s < cfg.substeps; ++s) {
             StateSet src = set[cur].view(), dst = set[cur ^ 1].view();
             KL(k_grid_reset<<<1, 1, 0, st>>>(ctl, 0));
             KL(k_list_reset<<<1, 1, 0, st>>>(ctl));
-            KL(k_predict<<<blocks(n, 256), 256, 0, st>>>(n, src.X, src.V, src.XS, dt, cfg.gravity[0],
-                                                      cfg.gravity[1], cfg.gravity[2], ctl, s));
-            ws.run_grid(0, src.XS, n, cfg.h, cfg.h, scene.n > 0, radius);
+            // substep 0 predicts into the backup set's V/x* so the frame-start
+            // state stays intact until a side stream has copied it (below)
+            StateSet pin = src;
+            if (s == 0) {
+                pin.V = backup.V.p;
+                pin.XS = backup.XS.p;
+                if (capturing) CK(cudaStreamWaitEvent(st, ev_vm, cudaEventWaitExternal));
+                else CK(cudaStreamWaitEvent(st, ev_vm, 0));
+            }
+            KL(k_predict<<<blocks(n, 256), 256, 0, st>>>(n, src.X, src.V, pin.V, src.XS, pin.XS, dt,
+                                                      cfg.gravity[0], cfg.gravity[1], cfg.gravity[2], ctl, s));
+            ws.run_grid(0, pin.XS, n, cfg.h, cfg.h, scene.n > 0, radius);
             const int smemG = (nMax + 1) * (int)sizeof(int);
-            KL(k_gather<<<numTiles, kTileThreads, smemG, st>>>(n, ctl, ws.perm.p, src, dst, nMax, numTiles,
+            if (s == 0) {
+                // a host stepFrame uploads inverse mass last (upload_split); a
+                // no-op wait when nothing was uploaded that way
+                if (capturing) CK(cudaStreamWaitEvent(st, ev_inputs, cudaEventWaitExternal));
+                else CK(cudaStreamWaitEvent(st, ev_inputs, 0));
+            } else if (s == 1) {
+                CK(cudaStreamWaitEvent(st, ev_bk_join, 0));  // backup taken before set[start] is overwritten
+            }
+            KL(k_gather<<<numTiles, kTileThreads, smemG, st>>>(n, ctl, ws.perm.p, pin, dst, nMax, numTiles,
                                                            tileCount.p));
+            if (s == 0) {
+                // frame-start state for a list-overflow retry (levels included:
+                // a retry's LOD recomputes the same ones from the same x), copied
+                // off the critical path while this substep runs
+                CK(cudaEventRecord(ev_bk_fork, st));
+                CK(cudaStreamWaitEvent(bk_stream, ev_bk_fork, 0));
+                copy_set(backup, set[cur], bk_stream);
+                CK(cudaEventRecord(ev_bk_join, bk_stream));
+                if (cfg.substeps == 1) CK(cudaStreamWaitEvent(st, ev_bk_join, 0));
+            }
             if (s == cfg.substeps - 1) rec(ev[7]);  // final storage order (overlapped download)
             KL(k_level_scan<<<nMax + 1, 1024, 0, st>>>(ctl, numTiles, tileCount.p, levelCount.p));
             KL(k_level_finish<<<1, 32, 0, st>>>(ctl, n, nMax, levelCount.p, activeCount.p, bucketStart.p));
@@ -1014,10 +1046,14 @@ struct apbf_gpu_solver {
     HostOut* host_out = nullptr;
     cudaStream_t copy_stream = nullptr;
     cudaEvent_t ev_x = nullptr, ev_inputs = nullptr;  // upload_split: x unpacked / everything unpacked
+    cudaEvent_t ev_vm = nullptr;                      // upload_split: v and mass unpacked
+    cudaEvent_t ev_bk_fork = nullptr, ev_bk_join = nullptr;  // frame-start backup on bk_stream
+    cudaStream_t bk_stream = nullptr;
 
     // The inputs of a host stepFrame: x on the solver stream (the LOD pass
     // needs only x), v, mass and inverse mass on copy_stream, unpacked there
-    // once x is; the frame waits for ev_inputs after its LOD pass.
+    // once x is; the frame waits for ev_vm before its first predict and for
+    // ev_inputs before its first reorder.
     void upload_split(int nn, const float* x, const float* v, const float* mass, const float* inv_mass) {
         n = nn;
         levels_valid = nn == 0;
@@ -1029,15 +1065,29 @@ struct apbf_gpu_solver {
         CK(cudaMemcpyAsync(d, x, n3, cudaMemcpyHostToDevice, st));
         KL(k_unpack_x<<<blocks(nn, 256), 256, 0, st>>>(nn, d, set[0].X.p));
         CK(cudaEventRecord(ev_x, st));
+        // v and mass (predict), then inverse mass (first reorder): the frame
+        // waits for each right where it first reads it
         CK(cudaMemcpyAsync(d + 6LL * nn, v, n3, cudaMemcpyHostToDevice, copy_stream));
         CK(cudaMemcpyAsync(d + 9LL * nn, mass, n1, cudaMemcpyHostToDevice, copy_stream));
-        CK(cudaMemcpyAsync(d + 10LL * nn, inv_mass, n1, cudaMemcpyHostToDevice, copy_stream));
         CK(cudaStreamWaitEvent(copy_stream, ev_x, 0));
-        KL(k_unpack_rest<<<blocks(nn, 256), 256, 0, copy_stream>>>(nn, d, set[0].view()));
+        KL(k_unpack_vm<<<blocks(nn, 256), 256, 0, copy_stream>>>(nn, d, set[0].view()));
+        CK(cudaEventRecord(ev_vm, copy_stream));
+        CK(cudaMemcpyAsync(d + 10LL * nn, inv_mass, n1, cudaMemcpyHostToDevice, copy_stream));
+        KL(k_unpack_w<<<blocks(nn, 256), 256, 0, copy_stream>>>(nn, d, set[0].view()));
         LAUNCH_CHECK();
         CK(cudaEventRecord(ev_inputs, copy_stream));
         w_agreed = false;
-        scan_inv_mass(nn, inv_mass);  // on the host while the copies run
+        // The inverse-mass mode picks the lambda variant, so it is part of the
+        // frame graph's key.  Scanning 4 B/particle on the host would delay the
+        // launch; once a mode is known the frame launches with it and the scan
+        // runs while the GPU works (finish_frame), re-running the frame in the
+        // rare case the mode changed.
+        if (w_known) {
+            pending_scan = inv_mass;
+        } else {
+            scan_inv_mass(nn, inv_mass);
+            w_known = true;
+        }
     }
 
     // The frame's result to the caller's arrays on `st`: the fields that are
@@ -1067,6 +1117,16 @@ struct apbf_gpu_solver {
             if (!copy_stream) CK(cudaStreamCreateWithFlags(&copy_stream, cudaStreamNonBlocking));
             enqueue_download(copy_stream, *host_out);
             host_out->queued = true;
+        }
+        if (pending_scan) {
+            // The download may be rewriting these very values in the frame's
+            // storage order meanwhile: a permutation of the same multiset, so
+            // the scan's answer does not depend on how far it got.
+            const int used = w_mode;
+            const float used_w0 = w0;
+            scan_inv_mass(n, pending_scan);
+            pending_scan = nullptr;
+            w_mismatch = w_mode != used || (w_mode == 2 && std::memcmp(&w0, &used_w0, sizeof w0) != 0);
         }
         CK(cudaStreamSynchronize(ws.stream));
         if (host_out && n > 0) CK(cudaStreamSynchronize(copy_stream));
@@ -1101,7 +1161,7 @@ struct apbf_gpu_solver {
                   (block_threads << 8);
         k.caps[0] = nbrCap;
         k.stride = list_stride;
-        std::memcpy(&k.w0bits, &w0, sizeof w0);
+        if (w_mode == 2) std::memcpy(&k.w0bits, &w0, sizeof w0);
         k.caps[1] = listCap16;
         k.caps[2] = fbCap;
         if (assign_lod && cam) k.cam = *cam;
@@ -1196,6 +1256,14 @@ struct apbf_gpu_solver {
         for (int attempt = 0;; ++attempt) {
             if (attempt == 0) launch_frame(assign_lod, cam, lod);
             else run_frame(assign_lod, cam, lod);
+            if (w_mismatch) {
+                // ran with the previous upload's inverse-mass mode: run again
+                w_mismatch = false;
+                cur = start_set;
+                copy_set(set[cur], backup);
+                --attempt;
+                continue;
+            }
             if (!ws.h_ctl->list_overflow) break;
             // Neighbour storage too small: restore the frame-start state,
             // double the capacity and run the frame again.
@@ -1379,6 +1447,8 @@ struct apbf_gpu_solver {
         if (level) CK(cudaMemcpyAsync(d + 12LL * nn, level, n1, cudaMemcpyHostToDevice, st));
         w_agreed = false;  // slab ranks agree on w_mode at their next frame
         scan_inv_mass(nn, inv_mass);  // on the host while the copies run
+        w_known = true;
+        pending_scan = nullptr;
         const int have = (xs ? 1 : 0) | (lambda ? 2 : 0) | (level ? 4 : 0);
         KL(k_unpack_state<<<blocks(nn, 256), 256, 0, st>>>(nn, d, set[0].view(), have));
         LAUNCH_CHECK();
@@ -1486,8 +1556,8 @@ struct apbf_gpu_solver {
             StateSet src = set[cur].view(), dst = set[cur ^ 1].view();
             KL(k_grid_reset<<<1, 1, 0, st>>>(ctl, 0));
             KL(k_list_reset<<<1, 1, 0, st>>>(ctl));
-            KL(k_predict<<<blocks(n, 256), 256, 0, st>>>(n, src.X, src.V, src.XS, dt, cfg.gravity[0],
-                                                      cfg.gravity[1], cfg.gravity[2], ctl, s));
+            KL(k_predict<<<blocks(n, 256), 256, 0, st>>>(n, src.X, src.V, src.V, src.XS, src.XS, dt,
+                                                      cfg.gravity[0], cfg.gravity[1], cfg.gravity[2], ctl, s));
             // global grid: AABB all-reduce (ordered ints), identical params
             // everywhere; the abort flag travels with it (one host sync)
             T.allreduce(&ctl->abort, 1, RType::I32, ROp::Max, st);
@@ -1917,17 +1987,51 @@ int32_t apbf_gpu_step_frame_host(apbf_gpu_solver* s, int32_t n, float* x, float*
         s->cur = 0;
         // what stepFrame reads, x first (the caller's arrays stay untouched
         // until this call returns, so no sync)
+        // APBF_E2E_TRACE=1: print where the end-to-end frame spends its time
+        static const bool trace = std::getenv("APBF_E2E_TRACE") != nullptr;
+        cudaEvent_t t0 = nullptr, t1 = nullptr;
+        auto h0 = std::chrono::steady_clock::now();
+        if (trace) {
+            CK(cudaEventCreate(&t0));
+            CK(cudaEventCreate(&t1));
+            CK(cudaEventRecord(t0, s->ws.stream));
+        }
         s->upload_split(n, x, v, mass, inv_mass);
+        auto h1 = std::chrono::steady_clock::now();
         apbf_gpu_solver::HostOut o{x, x_star, v, mass, inv_mass, lambda, level, false};
         s->host_out = &o;
         try {
             s->frame(true, cam, lod, frame_index, out);
         } catch (...) {
             s->host_out = nullptr;
+            if (s->pending_scan) {  // never scanned: the mode is unknown now
+                s->pending_scan = nullptr;
+                s->w_known = false;
+            }
             throw;
         }
         s->host_out = nullptr;
         s->levels_valid = true;
+        if (trace) {
+            CK(cudaEventRecord(t1, s->copy_stream));
+            CK(cudaEventSynchronize(t1));
+            auto h2 = std::chrono::steady_clock::now();
+            auto el = [&](cudaEvent_t e) {
+                float ms = -1.f;
+                cudaEventElapsedTime(&ms, t0, e);
+                return ms;
+            };
+            std::fprintf(stderr,
+                         "[e2e] host: upload_split %.3f ms, total %.3f ms | device from start: x %.3f, "
+                         "inputs %.3f, frame start %.3f, lod+backup %.3f, last reorder %.3f, finalize %.3f, "
+                         "metrics %.3f, download done %.3f ms\n",
+                         std::chrono::duration<double, std::milli>(h1 - h0).count(),
+                         std::chrono::duration<double, std::milli>(h2 - h0).count(), el(s->ev_x),
+                         el(s->ev_inputs), el(s->ev[0]), s->phase_timing ? el(s->ev[1]) : -1.f,
+                         el(s->ev[7]), el(s->ev[5]), el(s->ev[6]), el(t1));
+            cudaEventDestroy(t0);
+            cudaEventDestroy(t1);
+        }
     });
 }
 

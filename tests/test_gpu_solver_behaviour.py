@@ -327,3 +327,31 @@ def test_frame_inputs_only_upload_matches_full_upload():
     part.upload(b, frame_inputs_only=True)
     with pytest.raises(ValueError):
         part.step_frame_with_levels_resident(0)
+
+
+def test_host_step_frame_follows_inverse_mass_mode_changes():
+    """The host stepFrame launches with the previous upload's inverse-mass
+    mode and scans the new one while the GPU runs; when the mode changed
+    (uniform -> mixed -> non-finite -> uniform again with another value) the
+    frame runs again: every frame equals a fresh solver's, bit for bit."""
+    spec = S.build_scenario("dam_break", 4096 / 216000)
+    base = S.make_state(spec, 5)
+    states = [base.copy() for _ in range(4)]
+    states[1].inv_mass[::5] = np.float32(0.0)                      # mixed, finite
+    states[2].inv_mass[17] = np.float32(np.inf)                    # non-finite
+    states[3].inv_mass[:] = np.float32(2.0) * states[3].inv_mass  # uniform, new w0
+    states[3].mass[:] = np.float32(0.5) * states[3].mass
+    reused = Solver(spec.solver, spec.scene)
+    for f, st in enumerate(states + [base.copy()]):
+        a, b = st.copy(), st.copy()
+        errs = []
+        for sv, s in ((reused, a), (Solver(spec.solver, spec.scene), b)):
+            try:
+                sv.step_frame(s, spec.camera, spec.lod, f)
+                errs.append(None)
+            except NumericalError as e:
+                errs.append((e.pass_, e.particle))
+        assert errs[0] == errs[1], f
+        if errs[0] is None:
+            for k in ("x", "x_star", "v", "mass", "inv_mass", "lambda_", "level"):
+                assert np.array_equal(getattr(a, k), getattr(b, k)), (f, k)
