@@ -371,8 +371,13 @@ struct apbf_gpu_solver {
     Scene scene;
     Workspace ws;
     int n = 0;
-    SetBufs set[2];
-    SetBufs backup;
+    // Three state sets.  A single-rank frame never writes the set it starts
+    // from (predict of the first substep writes into the third set, whose
+    // buffers the second substep's reorder fills only afterwards), so a
+    // list-overflow retry restarts from it without a backup copy; successive
+    // frames rotate through the sets (one cached graph per start set).  The
+    // slab path alternates set[0]/set[1] and keeps its retry copy in set[2].
+    SetBufs set[3];
     int cur = 0;
     DBuf<float4> PB;
     DBuf<float4> PL;  // (x*, lambda) published by the lambda pass for the delta-p gathers
@@ -453,9 +458,6 @@ struct apbf_gpu_solver {
         CK(cudaEventCreateWithFlags(&ev_x, evf));
         CK(cudaEventCreateWithFlags(&ev_inputs, evf));
         CK(cudaEventCreateWithFlags(&ev_vm, evf));
-        CK(cudaEventCreateWithFlags(&ev_bk_fork, cudaEventDisableTiming));
-        CK(cudaEventCreateWithFlags(&ev_bk_join, cudaEventDisableTiming));
-        CK(cudaStreamCreateWithFlags(&bk_stream, cudaStreamNonBlocking));
         if (const char* v = std::getenv("APBF_STAGE_LISTS")) use_stage = std::atoi(v) != 0;
         if (const char* v = std::getenv("APBF_COEF_CACHE")) use_coef = std::atoi(v) != 0;
         if (const char* v = std::getenv("APBF_TILES")) use_tiles = std::atoi(v) != 0;
@@ -481,9 +483,6 @@ struct apbf_gpu_solver {
         for (auto& e : ev) cudaEventDestroy(e);
         if (ev_x) cudaEventDestroy(ev_x);
         if (ev_vm) cudaEventDestroy(ev_vm);
-        if (ev_bk_fork) cudaEventDestroy(ev_bk_fork);
-        if (ev_bk_join) cudaEventDestroy(ev_bk_join);
-        if (bk_stream) cudaStreamDestroy(bk_stream);
         if (ev_inputs) cudaEventDestroy(ev_inputs);
         if (copy_stream) cudaStreamDestroy(copy_stream);
     }
@@ -501,7 +500,7 @@ struct apbf_gpu_solver {
         const size_t m = (size_t)std::max(nn, 1);
         set[0].ensure(m);
         set[1].ensure(m);
-        backup.ensure(m);
+        set[2].ensure(m);
         PB.ensure(m);
         PL.ensure(m);
         if (post_pass()) {
@@ -544,9 +543,9 @@ struct apbf_gpu_solver {
         ws.ensure_cells();
     }
 
-    void copy_set(SetBufs& dst, SetBufs& src, cudaStream_t st = nullptr) {
+    void copy_set(SetBufs& dst, SetBufs& src) {
         const size_t m = (size_t)n;
-        if (!st) st = ws.stream;
+        cudaStream_t st = ws.stream;
         CK(cudaMemcpyAsync(dst.X.p, src.X.p, sizeof(float4) * m, cudaMemcpyDeviceToDevice, st));
         CK(cudaMemcpyAsync(dst.V.p, src.V.p, sizeof(float4) * m, cudaMemcpyDeviceToDevice, st));
         CK(cudaMemcpyAsync(dst.XS.p, src.XS.p, sizeof(float4) * m, cudaMemcpyDeviceToDevice, st));
@@ -892,16 +891,20 @@ struct apbf_gpu_solver {
             }
         }
         mark(1);
+        const int sa = cur, sb = (cur + 1) % 3, sc3 = (cur + 2) % 3;
         for (int s = 0; s < cfg.substeps; ++s) {
-            StateSet src = set[cur].view(), dst = set[cur ^ 1].view();
+            // substeps: a -> b, then b -> c, c -> b, ... (a is never written)
+            const int si = s == 0 ? sa : ((s & 1) ? sb : sc3);
+            const int di = s == 0 ? sb : ((s & 1) ? sc3 : sb);
+            StateSet src = set[si].view(), dst = set[di].view();
             KL(k_grid_reset<<<1, 1, 0, st>>>(ctl, 0));
             KL(k_list_reset<<<1, 1, 0, st>>>(ctl));
-            // substep 0 predicts into the backup set's V/x* so the frame-start
-            // state stays intact until a side stream has copied it (below)
+            // substep 0 predicts into the third set's V/x* (free until the
+            // next substep's reorder), keeping the start set intact
             StateSet pin = src;
             if (s == 0) {
-                pin.V = backup.V.p;
-                pin.XS = backup.XS.p;
+                pin.V = set[sc3].V.p;
+                pin.XS = set[sc3].XS.p;
                 if (capturing) CK(cudaStreamWaitEvent(st, ev_vm, cudaEventWaitExternal));
                 else CK(cudaStreamWaitEvent(st, ev_vm, 0));
             }
@@ -914,21 +917,9 @@ struct apbf_gpu_solver {
                 // no-op wait when nothing was uploaded that way
                 if (capturing) CK(cudaStreamWaitEvent(st, ev_inputs, cudaEventWaitExternal));
                 else CK(cudaStreamWaitEvent(st, ev_inputs, 0));
-            } else if (s == 1) {
-                CK(cudaStreamWaitEvent(st, ev_bk_join, 0));  // backup taken before set[start] is overwritten
             }
             KL(k_gather<<<numTiles, kTileThreads, smemG, st>>>(n, ctl, ws.perm.p, pin, dst, nMax, numTiles,
                                                            tileCount.p));
-            if (s == 0) {
-                // frame-start state for a list-overflow retry (levels included:
-                // a retry's LOD recomputes the same ones from the same x), copied
-                // off the critical path while this substep runs
-                CK(cudaEventRecord(ev_bk_fork, st));
-                CK(cudaStreamWaitEvent(bk_stream, ev_bk_fork, 0));
-                copy_set(backup, set[cur], bk_stream);
-                CK(cudaEventRecord(ev_bk_join, bk_stream));
-                if (cfg.substeps == 1) CK(cudaStreamWaitEvent(st, ev_bk_join, 0));
-            }
             if (s == cfg.substeps - 1) rec(ev[7]);  // final storage order (overlapped download)
             KL(k_level_scan<<<nMax + 1, 1024, 0, st>>>(ctl, numTiles, tileCount.p, levelCount.p));
             KL(k_level_finish<<<1, 32, 0, st>>>(ctl, n, nMax, levelCount.p, activeCount.p, bucketStart.p));
@@ -991,7 +982,7 @@ struct apbf_gpu_solver {
                     in_iteration = true;
                     obs_xs = Pn;
                     const int c = cur;
-                    cur ^= 1;  // expose dst as the current set to get_state
+                    cur = di;  // expose dst as the current set to get_state
                     observer(observer_user, s, it);
                     cur = c;
                     in_iteration = false;
@@ -1011,7 +1002,7 @@ struct apbf_gpu_solver {
                                                              cfg.vorticity_epsilon, cap, dst.V));
             }
             LAUNCH_CHECK();
-            cur ^= 1;
+            cur = di;
             mark(4);
         }
         rec(ev[5]);
@@ -1047,8 +1038,6 @@ struct apbf_gpu_solver {
     cudaStream_t copy_stream = nullptr;
     cudaEvent_t ev_x = nullptr, ev_inputs = nullptr;  // upload_split: x unpacked / everything unpacked
     cudaEvent_t ev_vm = nullptr;                      // upload_split: v and mass unpacked
-    cudaEvent_t ev_bk_fork = nullptr, ev_bk_join = nullptr;  // frame-start backup on bk_stream
-    cudaStream_t bk_stream = nullptr;
 
     // The inputs of a host stepFrame: x on the solver stream (the LOD pass
     // needs only x), v, mass and inverse mass on copy_stream, unpacked there
@@ -1113,20 +1102,19 @@ struct apbf_gpu_solver {
 
     // Wait for the enqueued frame (and its overlapped download, if any).
     void finish_frame() {
-        if (host_out && n > 0) {
-            if (!copy_stream) CK(cudaStreamCreateWithFlags(&copy_stream, cudaStreamNonBlocking));
-            enqueue_download(copy_stream, *host_out);
-            host_out->queued = true;
-        }
         if (pending_scan) {
-            // The download may be rewriting these very values in the frame's
-            // storage order meanwhile: a permutation of the same multiset, so
-            // the scan's answer does not depend on how far it got.
+            // while the GPU runs the frame, and before the download into the
+            // same host arrays is enqueued
             const int used = w_mode;
             const float used_w0 = w0;
             scan_inv_mass(n, pending_scan);
             pending_scan = nullptr;
             w_mismatch = w_mode != used || (w_mode == 2 && std::memcmp(&w0, &used_w0, sizeof w0) != 0);
+        }
+        if (host_out && n > 0 && !w_mismatch) {  // a mismatched frame is re-run, then downloaded
+            if (!copy_stream) CK(cudaStreamCreateWithFlags(&copy_stream, cudaStreamNonBlocking));
+            enqueue_download(copy_stream, *host_out);
+            host_out->queued = true;
         }
         CK(cudaStreamSynchronize(ws.stream));
         if (host_out && n > 0) CK(cudaStreamSynchronize(copy_stream));
@@ -1141,11 +1129,16 @@ struct apbf_gpu_solver {
         apbf_lod_config lod;
     };
     bool use_graphs = true;  // APBF_GRAPHS=0 disables
-    bool graph_ok = false, eager_seen = false;
-    GraphKey gkey{}, seen_key{};
-    cudaGraphExec_t gexec = nullptr;
-    size_t kt_used_graph = 0;
-    unsigned long long graph_kernels = 0;  // kernel nodes of the frame graph
+    bool eager_seen = false;  // seen[] holds keys of frames run eagerly since the last reset
+    struct FrameGraph {
+        GraphKey key;
+        cudaGraphExec_t exec;
+        size_t kt_used;
+        unsigned long long kernels;  // kernel nodes of the frame graph
+    };
+    std::vector<FrameGraph> graphs;  // one per start set (frames rotate through three)
+    std::vector<GraphKey> seen;
+    static constexpr size_t kMaxGraphs = 3;
 
     GraphKey make_key(bool assign_lod, const apbf_camera* cam, const apbf_lod_config* lod) const {
         GraphKey k;
@@ -1169,28 +1162,36 @@ struct apbf_gpu_solver {
         return k;
     }
     void drop_graph() {
-        if (gexec) cudaGraphExecDestroy(gexec);
-        gexec = nullptr;
-        graph_ok = false;
+        for (auto& g : graphs) cudaGraphExecDestroy(g.exec);
+        graphs.clear();
     }
+    // The set a frame starting from set a ends in (enqueue_frame's rotation).
+    int final_set(int a) const { return (a + ((cfg.substeps & 1) ? 1 : 2)) % 3; }
 
-    // One frame: replay the captured graph when nothing changed since the
-    // previous frame, capture it on the second frame with the same key, run
-    // eagerly otherwise (first frame, observer, configuration change).
+    // One frame: replay a captured graph when one matches the frame's key,
+    // capture it the second time a key comes up, run eagerly otherwise (first
+    // frames, observer, configuration change).
     void launch_frame(bool assign_lod, const apbf_camera* cam, const apbf_lod_config* lod) {
         const GraphKey key = make_key(assign_lod, cam, lod);
         const bool graphable = use_graphs && !observer;
         cudaStream_t st = ws.stream;
-        if (graphable && graph_ok && std::memcmp(&key, &gkey, sizeof key) == 0) {
-            CK(cudaGraphLaunch(gexec, st));
-            g_launches += graph_kernels;
-            cur = key.start ^ (cfg.substeps & 1);
-            kt_used = kt_used_graph;
-            finish_frame();
-            return;
-        }
-        if (graphable && eager_seen && std::memcmp(&key, &seen_key, sizeof key) == 0) {
-            drop_graph();
+        auto same = [&](const GraphKey& k) { return std::memcmp(&k, &key, sizeof key) == 0; };
+        if (!eager_seen) seen.clear();
+        if (graphable)
+            for (auto& g : graphs)
+                if (same(g.key)) {
+                    CK(cudaGraphLaunch(g.exec, st));
+                    g_launches += g.kernels;
+                    cur = final_set(key.start);
+                    kt_used = g.kt_used;
+                    finish_frame();
+                    return;
+                }
+        if (graphable && std::any_of(seen.begin(), seen.end(), same)) {
+            if (graphs.size() >= kMaxGraphs) {
+                cudaGraphExecDestroy(graphs.front().exec);
+                graphs.erase(graphs.begin());
+            }
             cudaGraph_t g = nullptr;
             CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
             const unsigned long long l0 = g_launches;
@@ -1205,21 +1206,20 @@ struct apbf_gpu_solver {
                 throw;
             }
             CK(cudaStreamEndCapture(st, &g));
-            graph_kernels = g_launches - l0;  // captured, not run: counted per replay
+            FrameGraph fg{key, nullptr, kt_used, g_launches - l0};  // captured, not run: counted per replay
             g_launches = l0;
-            CK(cudaGraphInstantiate(&gexec, g, 0));
+            CK(cudaGraphInstantiate(&fg.exec, g, 0));
             cudaGraphDestroy(g);
-            kt_used_graph = kt_used;
-            gkey = key;
-            graph_ok = true;
-            CK(cudaGraphLaunch(gexec, st));
-            g_launches += graph_kernels;
-            cur = key.start ^ (cfg.substeps & 1);
+            graphs.push_back(fg);
+            CK(cudaGraphLaunch(fg.exec, st));
+            g_launches += fg.kernels;
+            cur = final_set(key.start);
             finish_frame();
             return;
         }
         run_frame(assign_lod, cam, lod);
-        seen_key = key;
+        if (seen.size() >= kMaxGraphs) seen.erase(seen.begin());
+        seen.push_back(key);
         eager_seen = true;
     }
 
@@ -1258,18 +1258,18 @@ struct apbf_gpu_solver {
             else run_frame(assign_lod, cam, lod);
             if (w_mismatch) {
                 // ran with the previous upload's inverse-mass mode: run again
+                // from the (unwritten) start set
                 w_mismatch = false;
                 cur = start_set;
-                copy_set(set[cur], backup);
                 --attempt;
                 continue;
             }
             if (!ws.h_ctl->list_overflow) break;
-            // Neighbour storage too small: restore the frame-start state,
-            // double the capacity and run the frame again.
+            // Neighbour storage too small: double the capacity and run the
+            // frame again from the start set (levels included: a retry's LOD
+            // recomputes the same ones from the same x).
             if (attempt > 6) fail(APBF_ERR_RUNTIME, "neighbor list overflow");
             cur = start_set;
-            copy_set(set[cur], backup);
             grow_lists(ws.h_ctl->list_alloc, ws.h_ctl->list_alloc_fb);
             drop_graph();
             eager_seen = false;
@@ -1796,6 +1796,10 @@ struct apbf_gpu_solver {
         const int G = T.size(), g = T.rank();
         if (G > kMaxRanks) fail(APBF_ERR_INVALID_ARGUMENT, "too many slab ranks");
         if (observer) fail(APBF_ERR_INVALID_ARGUMENT, "iteration observer is not available with slab decomposition");
+        if (cur == 2) {  // left there by single-rank frames: the slab path alternates 0/1
+            copy_set(set[0], set[2]);
+            cur = 0;
+        }
         std::vector<long long> cnt = all_counts(T, n);
         long long nAll = 0;
         for (long long c : cnt) nAll += c;
@@ -1814,14 +1818,14 @@ struct apbf_gpu_solver {
         if (nAll > 0) {
             const int start_set = cur;
             const int start_n = n;
-            copy_set(backup, set[start_set]);
+            copy_set(set[2], set[start_set]);
             for (int attempt = 0;; ++attempt) {
                 run_frame_dist(T, cnt, assign_lod, cam, lod);
                 if (!ws.h_ctl->list_overflow) break;
                 if (attempt > 6) fail(APBF_ERR_RUNTIME, "neighbor list overflow");
                 cur = start_set;
                 n = start_n;
-                copy_set(set[cur], backup);
+                copy_set(set[cur], set[2]);
                 grow_lists(ws.h_ctl->list_alloc, ws.h_ctl->list_alloc_fb);
             }
             const Ctl& c = *ws.h_ctl;
@@ -2023,7 +2027,7 @@ int32_t apbf_gpu_step_frame_host(apbf_gpu_solver* s, int32_t n, float* x, float*
             };
             std::fprintf(stderr,
                          "[e2e] host: upload_split %.3f ms, total %.3f ms | device from start: x %.3f, "
-                         "inputs %.3f, frame start %.3f, lod+backup %.3f, last reorder %.3f, finalize %.3f, "
+                         "inputs %.3f, frame start %.3f, lod %.3f, last reorder %.3f, finalize %.3f, "
                          "metrics %.3f, download done %.3f ms\n",
                          std::chrono::duration<double, std::milli>(h1 - h0).count(),
                          std::chrono::duration<double, std::milli>(h2 - h0).count(), el(s->ev_x),
