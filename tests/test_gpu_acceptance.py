@@ -38,9 +38,9 @@ def test_criterion_3_wall_clock_reduction_at_1m():
     """C3 (time part): APBF's median frame time is below PBF at N_max -- on the
     BASELINE 1M ocean, APBF {5..10} vs PBF 10.  The reference's bar (>= 15% at
     27k particles on its CPU) does not transfer: on the B200 a 27k frame is
-    launch-bound, and at 1M the per-frame fixed cost (grid, lists, LOD, ~0.9
-    ms) dilutes the 23% work cut to a ~14% time cut (profiles/README.md, C4
-    sweep: 17.8% at N = 20).  Asserted here with margin: >= 5%."""
+    launch-bound, and at 1M the per-frame fixed cost (grid, lists, LOD, ~0.75
+    ms) dilutes the 24% work cut to a ~15% time cut (profiles/README.md, C4
+    sweep: 18.2% reduction at N = 20).  Asserted here with margin: >= 5%."""
     spec = S.build_scenario("ocean_1m")
     res = H.run_bench(spec, H.parse_bench_modes("pbf:10,apbf:dtc,apbf:dtvs"), 3, 10, 1)
     t_pbf = res[0].median_frame_ms
