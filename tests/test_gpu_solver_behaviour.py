@@ -355,3 +355,28 @@ def test_host_step_frame_follows_inverse_mass_mode_changes():
         if errs[0] is None:
             for k in ("x", "x_star", "v", "mass", "inv_mass", "lambda_", "level"):
                 assert np.array_equal(getattr(a, k), getattr(b, k)), (f, k)
+
+
+@pytest.mark.parametrize("substeps", [1, 2, 3])
+def test_state_set_rotation_and_graph_cache_bitwise(substeps):
+    """Frames rotate through three state sets (period 3) with one cached CUDA
+    Graph per start set: 10 resident frames and 3 host stepFrames (which
+    restart from set 0) with odd and even substep counts stay equal to the
+    oracle, bit for bit, through the eager, capture and replay phases."""
+    spec = S.build_scenario("dam_break", 4096 / 216000)
+    spec.solver.substeps = substeps
+    gpu, orc = Solver(spec.solver, spec.scene), O.OracleSolver(spec.solver, spec.scene)
+    a = S.make_state(spec, 4)
+    b = a.copy()
+    gpu.upload(a)
+    for f in range(10):
+        sa = gpu.step_frame_resident(spec.camera, spec.lod, f)
+        sb = orc.step_frame(b, spec.camera, spec.lod, f)
+        assert (sa.total_iterations, sa.contacts, sa.min_density_pct) == \
+            (sb.total_iterations, sb.contacts, sb.min_density_pct), f
+    gpu.download(a)
+    for f in range(10, 13):
+        gpu.step_frame(a, spec.camera, spec.lod, f)
+        orc.step_frame(b, spec.camera, spec.lod, f)
+    for k in ("x", "x_star", "v", "mass", "inv_mass", "lambda_", "level"):
+        assert np.array_equal(getattr(a, k), getattr(b, k)), k
