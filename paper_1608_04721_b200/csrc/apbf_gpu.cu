@@ -1168,52 +1168,68 @@ struct apbf_gpu_solver {
     // The set a frame starting from set a ends in (enqueue_frame's rotation).
     int final_set(int a) const { return (a + ((cfg.substeps & 1) ? 1 : 2)) % 3; }
 
-    // One frame: replay a captured graph when one matches the frame's key,
-    // capture it the second time a key comes up, run eagerly otherwise (first
-    // frames, observer, configuration change).
+    // One frame: replay a captured graph when one matches the frame's key;
+    // when the same configuration ran before (from any start set), capture the
+    // graphs of all three start sets (frames rotate through them) and launch
+    // this frame's; run eagerly otherwise (first frame, observer, changing
+    // configuration).
+    FrameGraph capture_graph(const GraphKey& key, bool assign_lod, const apbf_camera* cam,
+                             const apbf_lod_config* lod) {
+        cudaStream_t st = ws.stream;
+        const int c0 = cur;
+        cur = key.start;
+        cudaGraph_t g = nullptr;
+        CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+        const unsigned long long l0 = g_launches;
+        capturing = true;
+        try {
+            enqueue_frame(assign_lod, cam, lod);
+            capturing = false;
+        } catch (...) {
+            capturing = false;
+            cur = c0;
+            cudaStreamEndCapture(st, &g);
+            if (g) cudaGraphDestroy(g);
+            throw;
+        }
+        CK(cudaStreamEndCapture(st, &g));
+        FrameGraph fg{key, nullptr, kt_used, g_launches - l0};  // captured, not run: counted per replay
+        g_launches = l0;
+        cur = c0;
+        const cudaError_t e = cudaGraphInstantiate(&fg.exec, g, 0);
+        cudaGraphDestroy(g);
+        CK(e);
+        return fg;
+    }
     void launch_frame(bool assign_lod, const apbf_camera* cam, const apbf_lod_config* lod) {
         const GraphKey key = make_key(assign_lod, cam, lod);
         const bool graphable = use_graphs && !observer;
         cudaStream_t st = ws.stream;
         auto same = [&](const GraphKey& k) { return std::memcmp(&k, &key, sizeof key) == 0; };
+        auto same_config = [&](GraphKey k) {
+            k.start = key.start;
+            return same(k);
+        };
         if (!eager_seen) seen.clear();
-        if (graphable)
+        const FrameGraph* hit = nullptr;
+        if (graphable) {
             for (auto& g : graphs)
-                if (same(g.key)) {
-                    CK(cudaGraphLaunch(g.exec, st));
-                    g_launches += g.kernels;
-                    cur = final_set(key.start);
-                    kt_used = g.kt_used;
-                    finish_frame();
-                    return;
+                if (same(g.key)) hit = &g;
+            if (!hit && std::any_of(seen.begin(), seen.end(), same_config)) {
+                drop_graph();
+                for (int k = 0; k < 3; ++k) {
+                    GraphKey kk = key;
+                    kk.start = (key.start + k) % 3;
+                    graphs.push_back(capture_graph(kk, assign_lod, cam, lod));
                 }
-        if (graphable && std::any_of(seen.begin(), seen.end(), same)) {
-            if (graphs.size() >= kMaxGraphs) {
-                cudaGraphExecDestroy(graphs.front().exec);
-                graphs.erase(graphs.begin());
+                hit = &graphs.front();
             }
-            cudaGraph_t g = nullptr;
-            CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
-            const unsigned long long l0 = g_launches;
-            capturing = true;
-            try {
-                enqueue_frame(assign_lod, cam, lod);
-                capturing = false;
-            } catch (...) {
-                capturing = false;
-                cudaStreamEndCapture(st, &g);
-                if (g) cudaGraphDestroy(g);
-                throw;
-            }
-            CK(cudaStreamEndCapture(st, &g));
-            FrameGraph fg{key, nullptr, kt_used, g_launches - l0};  // captured, not run: counted per replay
-            g_launches = l0;
-            CK(cudaGraphInstantiate(&fg.exec, g, 0));
-            cudaGraphDestroy(g);
-            graphs.push_back(fg);
-            CK(cudaGraphLaunch(fg.exec, st));
-            g_launches += fg.kernels;
+        }
+        if (hit) {
+            CK(cudaGraphLaunch(hit->exec, st));
+            g_launches += hit->kernels;
             cur = final_set(key.start);
+            kt_used = hit->kt_used;
             finish_frame();
             return;
         }
