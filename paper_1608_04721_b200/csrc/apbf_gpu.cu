@@ -461,6 +461,7 @@ struct apbf_gpu_solver {
         if (const char* v = std::getenv("APBF_STAGE_LISTS")) use_stage = std::atoi(v) != 0;
         if (const char* v = std::getenv("APBF_COEF_CACHE")) use_coef = std::atoi(v) != 0;
         if (const char* v = std::getenv("APBF_TILES")) use_tiles = std::atoi(v) != 0;
+        if (const char* v = std::getenv("APBF_WSORT")) use_wsort = std::atoi(v) != 0;
         if (const char* v = std::getenv("APBF_C16")) use_c16 = std::atoi(v) != 0;
         if (post_pass()) {  // the post-pass walks the 32-bit per-particle lists
             use_c16 = false;
@@ -501,6 +502,14 @@ struct apbf_gpu_solver {
         set[0].ensure(m);
         set[1].ensure(m);
         set[2].ensure(m);
+        {
+            const unsigned long long g0 = g_alloc_gen;
+            cntA.ensure(m);
+            cntB.ensure(m);
+            orderPre.ensure(m);
+            dstpos.ensure(m);
+            if (g_alloc_gen != g0) CK(cudaMemsetAsync(cntA.p, 0, sizeof(int) * m, ws.stream));
+        }
         PB.ensure(m);
         PL.ensure(m);
         if (post_pass()) {
@@ -704,9 +713,15 @@ struct apbf_gpu_solver {
                 groupBase.p, nbrCap, nbr16.p, lbase.p));
         else
             KL(k_build_lists_direct<<<blocks(nn, kListThreads), kListThreads, 0, st>>>(
-                nn, ws.ctl.p, order.p, dst.XS, ws.cellCount.p, cfg.h, cfg.h * cfg.h, nbr.p, nbrCount.p,
-                groupBase.p, list_stride));
+                nn, ws.ctl.p, wsort_on() ? orderPre.p : order.p, dst.XS, ws.cellCount.p, cfg.h,
+                cfg.h * cfg.h, nbr.p, nbrCount.p, groupBase.p, list_stride, wsort_on() ? cntA.p : nullptr,
+                wsort_on() ? dstpos.p : nullptr));
     }
+    // window sort of the iteration order by list length (k_order_window_sort)
+    bool use_wsort = false;  // APBF_WSORT=1: measured slower (profiles/README.md)
+    bool wsort_on() const { return use_wsort && !use_c16 && !staged_lists && !use_tiles && !transport; }
+    DBuf<int> cntA, cntB;   // list lengths by storage index / carried through the reorder
+    DBuf<int> orderPre, dstpos;  // level order before the window sort; its sorted positions
     void launch_residual(int nn, int it, const float4* Pn, const SolverConsts& sc, double* out, int oB,
                          int oE) {
         cudaStream_t st = ws.stream;
@@ -919,7 +934,8 @@ struct apbf_gpu_solver {
                 else CK(cudaStreamWaitEvent(st, ev_inputs, 0));
             }
             KL(k_gather<<<numTiles, kTileThreads, smemG, st>>>(n, ctl, ws.perm.p, pin, dst, nMax, numTiles,
-                                                           tileCount.p));
+                                                           tileCount.p, wsort_on() ? cntA.p : nullptr,
+                                                           wsort_on() ? cntB.p : nullptr));
             if (s == cfg.substeps - 1) rec(ev[7]);  // final storage order (overlapped download)
             KL(k_level_scan<<<nMax + 1, 1024, 0, st>>>(ctl, numTiles, tileCount.p, levelCount.p));
             KL(k_level_finish<<<1, 32, 0, st>>>(ctl, n, nMax, levelCount.p, activeCount.p, bucketStart.p));
@@ -933,7 +949,11 @@ struct apbf_gpu_solver {
                         n, ctl, S, dst.LV, dst.XS, dst.X, ws.scene.p, radius, cfg.stab_iterations, s));
             } else {
                 KL(k_level_scatter<<<numTiles, kTileThreads, 9 * smemG, st>>>(
-                    n, ctl, dst.LV, nMax, numTiles, tileCount.p, bucketStart.p, order.p));
+                    n, ctl, dst.LV, nMax, numTiles, tileCount.p, bucketStart.p,
+                    wsort_on() ? orderPre.p : order.p));
+                if (wsort_on())
+                    KL(k_order_window_sort<<<blocks(n, kWSort), kWSort, 0, st>>>(
+                        n, ctl, orderPre.p, order.p, dstpos.p, dst.LV, cntB.p));
                 launch_build_lists(n, dst);
                 if (S > 1)
                     KL(k_prestabilize<<<blocks(n, 256), 256, 0, st>>>(n, ctl, activeCount.p, S, order.p,
@@ -1150,7 +1170,7 @@ struct apbf_gpu_solver {
         k.ptime = phase_timing;
         k.n = n;
         k.flags = (use_tiles ? 1 : 0) | (use_stage ? 2 : 0) | (use_coef ? 4 : 0) | (use_c16 ? 8 : 0) |
-                  (w_mode << 20) | (staged_lists ? 0x400000 : 0) | (chunk << 4) |
+                  (w_mode << 20) | (staged_lists ? 0x400000 : 0) | (use_wsort ? 0x800000 : 0) | (chunk << 4) |
                   (block_threads << 8);
         k.caps[0] = nbrCap;
         k.stride = list_stride;

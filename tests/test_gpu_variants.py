@@ -2,7 +2,8 @@
 Solver creation) must give the default path's frames bit for bit: compact
 16-bit lists with and without the coefficient cache, the coefficient cache
 itself, shared-memory list staging, the cell-tile solver, gather batch sizes,
-CTA size, eager launches instead of CUDA Graph replay.  Also the compact
+CTA size, eager launches instead of CUDA Graph replay, the iteration order
+window-sorted by list length.  Also the compact
 lists' range fallback and the list stride fallback."""
 import numpy as np
 import pytest
@@ -24,6 +25,7 @@ VARIANTS = [
     {"APBF_CHUNK": "8"},
     {"APBF_BLOCK": "256"},
     {"APBF_GRAPHS": "0"},
+    {"APBF_WSORT": "1"},
 ]
 
 
