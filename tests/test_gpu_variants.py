@@ -103,3 +103,14 @@ def test_dense_cluster_switches_to_allocated_list_slabs():
         assert np.array_equal(getattr(a, k), getattr(b, k)), k
     entries, _ = gpu.last_neighbor_stats()
     assert entries / a.count() > 100
+
+
+def test_host_xstar_equals_x_after_clean_frames():
+    """stepFrame on host arrays writes back x* == x bitwise after finalize
+    (x = x*, solver.hpp:347-356)."""
+    spec = spec_apbf(False)
+    sv = Solver(spec.solver, spec.scene)
+    st = S.make_state(spec, 1)
+    for f in range(3):
+        sv.step_frame(st, spec.camera, spec.lod, f)
+        assert np.array_equal(st.x, st.x_star)
