@@ -18,6 +18,14 @@
 #include "apbf_dist.cuh"
 #include "apbf_transport.h"
 
+// CTA size of the passes that fold an AABB into the control block (predict,
+// aabb): one block-reduced atomic per coordinate bound per CTA, so large
+// CTAs (predict 28 -> 18 us, aabb 18 -> 11 us per 1M-particle launch, ncu)
+#ifndef APBF_AABB_BLOCK
+#define APBF_AABB_BLOCK 1024
+#endif
+static constexpr int kAabbBlock = APBF_AABB_BLOCK;
+
 #include <memory>
 #include <functional>
 #include <thread>
@@ -923,7 +931,7 @@ struct apbf_gpu_solver {
                 if (capturing) CK(cudaStreamWaitEvent(st, ev_vm, cudaEventWaitExternal));
                 else CK(cudaStreamWaitEvent(st, ev_vm, 0));
             }
-            KL(k_predict<<<blocks(n, 256), 256, 0, st>>>(n, src.X, src.V, pin.V, src.XS, pin.XS, dt,
+            KL(k_predict<<<blocks(n, kAabbBlock), kAabbBlock, 0, st>>>(n, src.X, src.V, pin.V, src.XS, pin.XS, dt,
                                                       cfg.gravity[0], cfg.gravity[1], cfg.gravity[2], ctl, s));
             ws.run_grid(0, pin.XS, n, cfg.h, cfg.h, scene.n > 0, radius);
             const int smemG = (nMax + 1) * (int)sizeof(int);
@@ -1029,7 +1037,7 @@ struct apbf_gpu_solver {
         if (metrics) {
             // allDensities(x) over a throwaway grid (solver.hpp:271-279).
             KL(k_grid_reset<<<1, 1, 0, st>>>(ctl, 1));
-            KL(k_aabb<<<blocks(n, 256), 256, 0, st>>>(n, set[cur].X.p, ctl, 1));
+            KL(k_aabb<<<blocks(n, kAabbBlock), kAabbBlock, 0, st>>>(n, set[cur].X.p, ctl, 1));
             ws.run_grid(1, set[cur].X.p, n, cfg.h, cfg.h, false, radius);
             KL(k_gather_posmass<<<blocks(n, 256), 256, 0, st>>>(n, ctl, ws.perm.p, set[cur].X.p,
                                                              set[cur].XS.p, sortedPM.p));
@@ -1592,7 +1600,7 @@ struct apbf_gpu_solver {
             StateSet src = set[cur].view(), dst = set[cur ^ 1].view();
             KL(k_grid_reset<<<1, 1, 0, st>>>(ctl, 0));
             KL(k_list_reset<<<1, 1, 0, st>>>(ctl));
-            KL(k_predict<<<blocks(n, 256), 256, 0, st>>>(n, src.X, src.V, src.V, src.XS, src.XS, dt,
+            KL(k_predict<<<blocks(n, kAabbBlock), kAabbBlock, 0, st>>>(n, src.X, src.V, src.V, src.XS, src.XS, dt,
                                                       cfg.gravity[0], cfg.gravity[1], cfg.gravity[2], ctl, s));
             // global grid: AABB all-reduce (ordered ints), identical params
             // everywhere; the abort flag travels with it (one host sync)
@@ -1751,7 +1759,7 @@ struct apbf_gpu_solver {
         Ctl* ctl = ws.ctl.p;
         const StateSet cs = set[cur].view();
         KL(k_grid_reset<<<1, 1, 0, st>>>(ctl, 1));
-        KL(k_aabb<<<blocks(n, 256), 256, 0, st>>>(n, cs.X, ctl, 1));
+        KL(k_aabb<<<blocks(n, kAabbBlock), kAabbBlock, 0, st>>>(n, cs.X, ctl, 1));
         T.allreduce(&ctl->grid[1].lo_ord[0], 3, RType::I32, ROp::Min, st);
         T.allreduce(&ctl->grid[1].hi_ord[0], 3, RType::I32, ROp::Max, st);
         KL(k_grid_params<<<1, 1, 0, st>>>(ctl, 1, cfg.h, cfg.h));
@@ -2216,7 +2224,7 @@ static void component_grid(Workspace& ws, int g, int n, float h, float pad) {
     cudaStream_t st = ws.stream;
     KL(k_frame_begin<<<1, 1, 0, st>>>(ws.ctl.p));
     KL(k_grid_reset<<<1, 1, 0, st>>>(ws.ctl.p, g));
-    KL(k_aabb<<<blocks(n, 256), 256, 0, st>>>(n, ws.tmp4.p, ws.ctl.p, g));
+    KL(k_aabb<<<blocks(n, kAabbBlock), kAabbBlock, 0, st>>>(n, ws.tmp4.p, ws.ctl.p, g));
     ws.run_grid(g, ws.tmp4.p, n, h, pad, false, 0.f);
     ws.read_ctl();
     if (ws.h_ctl->runtime_error) fail(APBF_ERR_RUNTIME, "grid cell count exceeds limit; domain blew up");
