@@ -920,8 +920,7 @@ struct apbf_gpu_solver {
             const int si = s == 0 ? sa : ((s & 1) ? sb : sc3);
             const int di = s == 0 ? sb : ((s & 1) ? sc3 : sb);
             StateSet src = set[si].view(), dst = set[di].view();
-            KL(k_grid_reset<<<1, 1, 0, st>>>(ctl, 0));
-            KL(k_list_reset<<<1, 1, 0, st>>>(ctl));
+            KL(k_substep_reset<<<1, 1, 0, st>>>(ctl));
             // substep 0 predicts into the third set's V/x* (free until the
             // next substep's reorder), keeping the start set intact
             StateSet pin = src;
@@ -1598,8 +1597,7 @@ struct apbf_gpu_solver {
         for (int s = 0; s < cfg.substeps; ++s) {
             localPre[s] = n;
             StateSet src = set[cur].view(), dst = set[cur ^ 1].view();
-            KL(k_grid_reset<<<1, 1, 0, st>>>(ctl, 0));
-            KL(k_list_reset<<<1, 1, 0, st>>>(ctl));
+            KL(k_substep_reset<<<1, 1, 0, st>>>(ctl));
             KL(k_predict<<<blocks(n, kAabbBlock), kAabbBlock, 0, st>>>(n, src.X, src.V, src.V, src.XS, src.XS, dt,
                                                       cfg.gravity[0], cfg.gravity[1], cfg.gravity[2], ctl, s));
             // global grid: AABB all-reduce (ordered ints), identical params
