@@ -294,6 +294,13 @@ int32_t apbf_gpu_neighbor_lists(int32_t n, const float* positions, float h, floa
 int32_t apbf_gpu_all_densities(int32_t n, const float* positions, const float* masses, float h,
                                float* rho_out, apbf_error* err);
 
+/* Not in the reference: the vorticity estimate of the
+ * opt-in post-pass, omega_i = sum_j (v_i - v_j) x gradW(x_i - x_j) over the
+ * strict r^2 < h^2 neighbours (Macklin & Mueller 2013 eq. 15), for n
+ * positions/velocities (xyz interleaved); omega_out (3n) in input order. */
+int32_t apbf_gpu_vorticity(int32_t n, const float* positions, const float* velocities, float h,
+                           float* omega_out, apbf_error* err);
+
 /* lodDtc (lod.hpp:83-104) and lodDtvs (lod.hpp:109-156); the level range is
  * taken from lod->n_min/n_max. */
 int32_t apbf_gpu_lod_dtc(int32_t n, const float* positions, const apbf_camera* cam,

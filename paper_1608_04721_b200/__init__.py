@@ -4,11 +4,11 @@ this package is the host mirror of /root/reference/proj/include/apbf/."""
 from .api import (Box, Camera, Cone, CudaError, FrameStats, HalfSpace, IterationRange, LodModel,
                   LodModelConfig, NumericalError, ParticleSet, SdfScene, Solver, SolverConfig,
                   SolverMode, Sphere, all_densities, blend_lod, count_contacts, grid_build, lod_dtc, lod_dtvs,
-                  neighbor_lists, read_ppm, render_level_image, splat, write_particle_snapshot,
-                  write_ppm)
+                  neighbor_lists, read_ppm, render_level_image, splat, vorticity,
+                  write_particle_snapshot, write_ppm)
 
 __all__ = ["Box", "Camera", "Cone", "CudaError", "FrameStats", "HalfSpace", "IterationRange",
            "LodModel", "LodModelConfig", "NumericalError", "ParticleSet", "SdfScene", "Solver",
            "SolverConfig", "SolverMode", "Sphere", "all_densities", "blend_lod", "count_contacts", "grid_build",
            "lod_dtc", "lod_dtvs", "neighbor_lists", "read_ppm", "render_level_image", "splat",
-           "write_particle_snapshot", "write_ppm"]
+           "vorticity", "write_particle_snapshot", "write_ppm"]

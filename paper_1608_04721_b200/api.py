@@ -645,6 +645,21 @@ def all_densities(positions, masses, h: float) -> np.ndarray:
     return rho[:p.shape[0]]
 
 
+def vorticity(positions, velocities, h: float) -> np.ndarray:
+    """The post-pass vorticity estimate (Macklin & Mueller 2013 eq. 15; not in
+    the reference), (n, 3) in input order."""
+    lib = capi.lib()
+    p = _pos(positions)
+    v = _pos(velocities)
+    if v.shape != p.shape:
+        raise ValueError("positions and velocities must have the same shape")
+    out = np.zeros((max(1, p.shape[0]), 3), F32)
+    err = capi.apbf_error()
+    rc = lib.apbf_gpu_vorticity(p.shape[0], _fp(p), _fp(v), h, _fp(out), C.byref(err))
+    raise_for(rc, err)
+    return out[:p.shape[0]]
+
+
 def lod_dtc(positions, cam: Camera, cfg: LodModelConfig) -> np.ndarray:
     """lodDtc (lod.hpp:83-104)."""
     lib = capi.lib()

@@ -12,8 +12,6 @@
 #include <vector>
 #include <array>
 
-#include "apbf_tiles.cuh"
-#include "apbf_c16.cuh"
 #include "apbf_post.cuh"
 #include "apbf_dist.cuh"
 #include "apbf_transport.h"
@@ -149,6 +147,7 @@ struct Workspace {
     DBuf<int> cellCount;   // kMaxCells + 1 (cellStart after the scan)
     DBuf<int> partial;
     DBuf<int> key, slot, bucket, perm;
+    DBuf<int> heavy;  // cells with > kRankDirect members (k_heavy_sort)
     DBuf<Scene> scene;
     DBuf<RadixSel> rs;
     DBuf<int> depth;
@@ -177,6 +176,7 @@ struct Workspace {
         slot.ensure(n);
         bucket.ensure(n);
         perm.ensure(n);
+        heavy.ensure(n / (kRankDirect + 1) + 1);
     }
     void ensure_cells() { cellCount.ensure((size_t)kMaxCells + 1); }
 
@@ -194,8 +194,9 @@ struct Workspace {
         KL(k_scan_apply<<<kScanGrid, kScanBlock, 0, stream>>>(ctl.p, g, cellCount.p, partial.p));
         KL(k_bucket_fill<<<blocks(n, 256), 256, 0, stream>>>(n, ctl.p, key.p, slot.p, cellCount.p,
                                                           bucket.p));
-        KL(k_stable_rank<<<blocks(n, 256), 256, 0, stream>>>(n, ctl.p, key.p, cellCount.p, bucket.p,
-                                                          perm.p));
+        KL(k_stable_rank<<<blocks(n, 256), 256, 0, stream>>>(n, ctl.p, key.p, slot.p, cellCount.p, bucket.p,
+                                                          perm.p, heavy.p));
+        KL(k_heavy_sort<<<148, kHeavyThreads, 0, stream>>>(n, ctl.p, heavy.p, cellCount.p, bucket.p, perm.p));
         LAUNCH_CHECK();
     }
 
@@ -391,18 +392,7 @@ struct apbf_gpu_solver {
     DBuf<float4> PL;  // (x*, lambda) published by the lambda pass for the delta-p gathers
     DBuf<int> order, nbrCount, nbr, tileCount, levelCount, activeCount, bucketStart;
     DBuf<long long> groupBase;
-    DBuf<float> coef;  // per-list-entry spiky coefficient, lambda -> delta-p (32-bit lists)
-    DBuf<unsigned short> nbr16;  // compact lists (APBF_C16=1)
-    DBuf<int4> lbase;            // compact lists: 3 layer bases + count per order position
     DBuf<int> lvTmp;             // multi-camera frames: one camera's levels before the blend
-    // cell-tile solver (apbf_tiles.cuh)
-    DBuf<TileInfo> tileInfo;
-    DBuf<int2> tileRuns;
-    DBuf<int> tileMax, fbLists;
-    DBuf<unsigned short> lists16;
-    DBuf<float> coef16;
-    long long listCap16 = 0, fbCap = 0;
-    int numTilesP = 0;
     DBuf<float4> sortedPM;
     DBuf<float> stage;  // compact host<->device staging (13 words per particle)
     DBuf<double> resid;
@@ -466,20 +456,7 @@ struct apbf_gpu_solver {
         CK(cudaEventCreateWithFlags(&ev_x, evf));
         CK(cudaEventCreateWithFlags(&ev_inputs, evf));
         CK(cudaEventCreateWithFlags(&ev_vm, evf));
-        if (const char* v = std::getenv("APBF_STAGE_LISTS")) use_stage = std::atoi(v) != 0;
-        if (const char* v = std::getenv("APBF_COEF_CACHE")) use_coef = std::atoi(v) != 0;
-        if (const char* v = std::getenv("APBF_TILES")) use_tiles = std::atoi(v) != 0;
-        if (const char* v = std::getenv("APBF_WSORT")) use_wsort = std::atoi(v) != 0;
-        if (const char* v = std::getenv("APBF_C16")) use_c16 = std::atoi(v) != 0;
-        if (post_pass()) {  // the post-pass walks the 32-bit per-particle lists
-            use_c16 = false;
-            use_tiles = false;
-        }
-        if (const char* v = std::getenv("APBF_BLOCK")) block_threads = std::atoi(v);
-        if (const char* v = std::getenv("APBF_CHUNK")) chunk = std::atoi(v);
         if (const char* v = std::getenv("APBF_GRAPHS")) use_graphs = std::atoi(v) != 0;
-        if (chunk != 1 && chunk != 2 && chunk != 8) chunk = 4;
-        if (block_threads != 256) block_threads = 128;
         configure_carveouts();
         CK(cudaMemcpy(ws.scene.p, &scene, sizeof(Scene), cudaMemcpyHostToDevice));
         levelCount.ensure(cfg.n_max + 2);
@@ -510,14 +487,6 @@ struct apbf_gpu_solver {
         set[0].ensure(m);
         set[1].ensure(m);
         set[2].ensure(m);
-        {
-            const unsigned long long g0 = g_alloc_gen;
-            cntA.ensure(m);
-            cntB.ensure(m);
-            orderPre.ensure(m);
-            dstpos.ensure(m);
-            if (g_alloc_gen != g0) CK(cudaMemsetAsync(cntA.p, 0, sizeof(int) * m, ws.stream));
-        }
         PB.ensure(m);
         PL.ensure(m);
         if (post_pass()) {
@@ -528,31 +497,13 @@ struct apbf_gpu_solver {
         const size_t groups = (m + 31) / 32 + 1;
         nbrCount.ensure(groups * 32);
         groupBase.ensure(groups);
-        lbase.ensure(groups * 32);
         list_groups = (long long)groups;
-        const long long need = (use_c16 || staged_lists) ? (long long)m * 48 + 4096
-                                                         : list_groups * list_stride * 32;
+        const long long need = packed_lists ? (long long)m * 48 + 4096 : list_groups * list_stride * 32;
         if (nbrCap < need) {
             nbrCap = need;
             alloc_lists();
         }
         numTiles = (int)((m + kTileSize - 1) / kTileSize);
-        numTilesP = (int)((m + kTileP - 1) / kTileP);
-        tileInfo.ensure(numTilesP);
-        tileRuns.ensure((size_t)numTilesP * kMaxRuns);
-        tileMax.ensure(numTilesP);
-        if (listCap16 < (long long)numTilesP * kTileP * 48) {
-            listCap16 = (long long)numTilesP * kTileP * 48;
-            lists16.release();
-            lists16.ensure((size_t)listCap16);
-            coef16.release();
-            coef16.ensure((size_t)listCap16);
-        }
-        if (fbCap < 64 * 1024) {
-            fbCap = 64 * 1024;
-            fbLists.release();
-            fbLists.ensure((size_t)fbCap);
-        }
         tileCount.ensure((size_t)(cfg.n_max + 1) * numTiles);
         sortedPM.ensure(m);
         stage.ensure(13 * m);
@@ -587,13 +538,6 @@ struct apbf_gpu_solver {
         return sc;
     }
 
-    // Variant switches for A/B measurements: APBF_STAGE_LISTS=1 stages list
-    // slabs in shared memory (bulk async copy); APBF_COEF_CACHE=1 has the
-    // lambda pass store every pair's spiky coefficient for delta-p instead of
-    // delta-p recomputing it with the exact fast sqrt/division (streaming 4 B
-    // per pair each way costs more than the ~20 instructions it saves).
-    // Every variant is bit-identical.
-    bool use_stage = false, use_coef = false, use_tiles = false;
     // every particle has the same inverse mass w0 (bitwise; checked at upload,
     // frames only permute it); single-GPU only -- a slab rank cannot see its ghosts'
     // what the uploaded inverse masses allow k_lambda to assume (its kW): 0
@@ -636,249 +580,118 @@ struct apbf_gpu_solver {
         if (w_mode == 2) std::memcpy(&w0, &h[1], sizeof w0);
         w_agreed = true;
     }
-    bool use_c16 = false;  // APBF_C16=1: compact 16-bit lists (slower here: the passes are latency-bound)
     // opt-in PBF velocity post-pass (config xsph_viscosity / vorticity_epsilon)
     bool post_pass() const { return cfg.xsph_viscosity != 0.0f || cfg.vorticity_epsilon != 0.0f; }
     DBuf<float4> postOm, postV;
-    // 32-bit lists: rows per lane of every warp slab (k_build_lists_direct);
-    // grows on overflow, never shrinks
+    // rows per lane of every warp slab (k_build_lists_direct); grows on
+    // overflow, never shrinks
     int list_stride = 64;
     long long list_groups = 0;
     // lists longer than this make the uniform stride too wasteful: fall back
-    // to k_build_lists<false> (per-warp slabs from an atomic allocator)
+    // to k_build_lists (per-warp slabs from an atomic allocator)
     static constexpr int kMaxListStride = 128;
-    bool staged_lists = false;
-    int block_threads = 128;  // APBF_BLOCK: CTA size of the order-based passes
-    int chunk = 4;            // APBF_CHUNK: neighbours gathered per batch (1, 2, 4, 8)
+    bool packed_lists = false;
     int ownB_ = 0, ownE_ = 0x7fffffff;  // owned slot range (slab mode); everything otherwise
     int n_iter = 0;                     // particles the solver passes cover (n, or owned+ghosts)
 
-    template <bool kZ, bool kS, bool kC, int kBT, int kK>
-    void launch_pair_btk(int it, int s, const float4* Pc, float4* Pn, const StateSet& dst,
-                         const SolverConsts& sc, int tslot) {
-        cudaStream_t st = ws.stream;
-        Ctl* ctl = ws.ctl.p;
-        const int sb = blocks(n_iter, kBT);
-        const int smem = kS ? kSolverSmem : 0;
-        // inverse-mass specialisations (w_mode) only for the default variant
-        if constexpr (!kS && kK == 4) {
-            if (w_mode == 2)
-                KL(k_lambda<kS, kC, kBT, kK, kZ, 2><<<sb, kBT, smem, st>>>(
-                    n_iter, it, ctl, activeCount.p, order.p, Pc, dst.W, dst.L, nbr.p, nbrCount.p,
-                    groupBase.p, coef.p, sc, s, ownB_, ownE_, PL.p));
-            else if (w_mode == 1)
-                KL(k_lambda<kS, kC, kBT, kK, kZ, 1><<<sb, kBT, smem, st>>>(
-                    n_iter, it, ctl, activeCount.p, order.p, Pc, dst.W, dst.L, nbr.p, nbrCount.p,
-                    groupBase.p, coef.p, sc, s, ownB_, ownE_, PL.p));
-            else
-                KL(k_lambda<kS, kC, kBT, kK, kZ><<<sb, kBT, smem, st>>>(
-                    n_iter, it, ctl, activeCount.p, order.p, Pc, dst.W, dst.L, nbr.p, nbrCount.p,
-                    groupBase.p, coef.p, sc, s, ownB_, ownE_, PL.p));
-        } else {
-            KL(k_lambda<kS, kC, kBT, kK, kZ><<<sb, kBT, smem, st>>>(n_iter, it, ctl, activeCount.p, order.p, Pc,
-                                                                 dst.W, dst.L, nbr.p, nbrCount.p, groupBase.p,
-                                                                 coef.p, sc, s, ownB_, ownE_, PL.p));
-        }
-        if (tslot >= 0) rec(kt_ev[tslot][1]);
-        // delta-p runs best in 256-thread CTAs, lambda in 128 (measured)
-        constexpr int kDB = (!kS && kBT == 128) ? 256 : kBT;
-        KL(k_deltap_apply<kZ, kS, kC, kDB, kK><<<blocks(n_iter, kDB), kDB, smem, st>>>(
-            n_iter, it, ctl, activeCount.p, order.p, Pc, Pn, dst.W, dst.L, dst.LV, nbr.p, nbrCount.p,
-            groupBase.p, coef.p, ws.scene.p, sc, s, ownB_, ownE_, PL.p));
-    }
+    // CTA sizes of the two solver passes (measured: lambda runs best in
+    // 128-thread CTAs, delta-p in 256) and the neighbour gathers in flight
+    // per batch.
+    static constexpr int kLambdaThreads = 128, kDeltapThreads = 256, kBatch = 4;
 
-    template <bool kZ, int kBT, int kK, bool kC>
-    void launch_pair_c16(int it, int s, const float4* Pc, float4* Pn, const StateSet& dst,
-                         const SolverConsts& sc, int tslot) {
-        cudaStream_t st = ws.stream;
-        Ctl* ctl = ws.ctl.p;
-        const int sb = blocks(n_iter, kBT);
-        KL(k_lambda_c16<kBT, kK, kZ, kC><<<sb, kBT, 0, st>>>(n_iter, it, ctl, activeCount.p, order.p, Pc, dst.W,
-                                                             dst.L, nbr16.p, lbase.p, groupBase.p, sc, s, ownB_,
-                                                             ownE_, PL.p, coef.p));
-        if (tslot >= 0) rec(kt_ev[tslot][1]);
-        KL(k_deltap_c16<kBT, kK, kC><<<sb, kBT, 0, st>>>(n_iter, it, ctl, activeCount.p, order.p, Pc, Pn, dst.W,
-                                                         dst.L, nbr16.p, lbase.p, groupBase.p, ws.scene.p, sc, s,
-                                                         ownB_, ownE_, PL.p, coef.p));
-    }
-    template <bool kZ, bool kC>
-    void launch_pair_c16_t(int it, int s, const float4* Pc, float4* Pn, const StateSet& dst,
-                           const SolverConsts& sc, int tslot) {
-        if (block_threads == 256) launch_pair_c16<kZ, 256, 4, kC>(it, s, Pc, Pn, dst, sc, tslot);
-        else launch_pair_c16<kZ, 128, 4, kC>(it, s, Pc, Pn, dst, sc, tslot);
-    }
-
-    // The list build and the residual pass for the current list encoding.
-    void launch_build_lists(int nn, const StateSet& dst) {
-        cudaStream_t st = ws.stream;
-        if (use_c16)
-            KL(k_build_lists<true><<<blocks(nn, kListThreads), kListThreads, 0, st>>>(
-                nn, ws.ctl.p, order.p, dst.XS, ws.cellCount.p, cfg.h, cfg.h * cfg.h, nbr.p, nbrCount.p,
-                groupBase.p, nbrCap, nbr16.p, lbase.p));
-        else if (staged_lists)
-            KL(k_build_lists<false><<<blocks(nn, kListThreads), kListThreads, 0, st>>>(
-                nn, ws.ctl.p, order.p, dst.XS, ws.cellCount.p, cfg.h, cfg.h * cfg.h, nbr.p, nbrCount.p,
-                groupBase.p, nbrCap, nbr16.p, lbase.p));
-        else
-            KL(k_build_lists_direct<<<blocks(nn, kListThreads), kListThreads, 0, st>>>(
-                nn, ws.ctl.p, wsort_on() ? orderPre.p : order.p, dst.XS, ws.cellCount.p, cfg.h,
-                cfg.h * cfg.h, nbr.p, nbrCount.p, groupBase.p, list_stride, wsort_on() ? cntA.p : nullptr,
-                wsort_on() ? dstpos.p : nullptr));
-    }
-    // window sort of the iteration order by list length (k_order_window_sort)
-    bool use_wsort = false;  // APBF_WSORT=1: measured slower (profiles/README.md)
-    bool wsort_on() const { return use_wsort && !use_c16 && !staged_lists && !use_tiles && !transport; }
-    DBuf<int> cntA, cntB;   // list lengths by storage index / carried through the reorder
-    DBuf<int> orderPre, dstpos;  // level order before the window sort; its sorted positions
-    void launch_residual(int nn, int it, const float4* Pn, const SolverConsts& sc, double* out, int oB,
-                         int oE) {
-        cudaStream_t st = ws.stream;
-        if (use_c16)
-            KL(k_residual<true><<<blocks(nn, 256), 256, 0, st>>>(nn, it, ws.ctl.p, activeCount.p, order.p, Pn,
-                                                                 nbr.p, nbrCount.p, groupBase.p, sc, out, oB,
-                                                                 oE, nbr16.p, lbase.p));
-        else
-            KL(k_residual<false><<<blocks(nn, 256), 256, 0, st>>>(nn, it, ws.ctl.p, activeCount.p, order.p,
-                                                                  Pn, nbr.p, nbrCount.p, groupBase.p, sc, out,
-                                                                  oB, oE, nbr16.p, lbase.p));
-    }
-
-    template <bool kZ, bool kS, bool kC, int kBT>
-    void launch_pair_bt(int it, int s, const float4* Pc, float4* Pn, const StateSet& dst,
-                        const SolverConsts& sc, int tslot) {
-        if (kS || chunk == 1) launch_pair_btk<kZ, kS, kC, kBT, 1>(it, s, Pc, Pn, dst, sc, tslot);
-        else if (chunk == 2) launch_pair_btk<kZ, kS, kC, kBT, 2>(it, s, Pc, Pn, dst, sc, tslot);
-        else if (chunk == 4) launch_pair_btk<kZ, kS, kC, kBT, 4>(it, s, Pc, Pn, dst, sc, tslot);
-        else launch_pair_btk<kZ, kS, kC, kBT, 8>(it, s, Pc, Pn, dst, sc, tslot);
-    }
-
-    template <bool kZ, bool kS, bool kC>
+    template <bool kZ>
     void launch_pair_t(int it, int s, const float4* Pc, float4* Pn, const StateSet& dst,
                        const SolverConsts& sc, int tslot) {
-        if (kS || block_threads != 256) launch_pair_bt<kZ, kS, kC, 128>(it, s, Pc, Pn, dst, sc, tslot);
-        else launch_pair_bt<kZ, kS, kC, 256>(it, s, Pc, Pn, dst, sc, tslot);
-    }
-
-    // The gather passes want L1, not shared memory (they use none unless
-    // list staging is on).
-    template <int kBT>
-    static void carveout_bt() {
-        const int a = cudaSharedmemCarveoutMaxL1;
-        cudaFuncSetAttribute(k_lambda<false, true, kBT>, cudaFuncAttributePreferredSharedMemoryCarveout, a);
-        cudaFuncSetAttribute(k_lambda<false, false, kBT>, cudaFuncAttributePreferredSharedMemoryCarveout, a);
-        cudaFuncSetAttribute(k_deltap_apply<false, false, true, kBT>,
-                             cudaFuncAttributePreferredSharedMemoryCarveout, a);
-        cudaFuncSetAttribute(k_deltap_apply<false, false, false, kBT>,
-                             cudaFuncAttributePreferredSharedMemoryCarveout, a);
-        cudaFuncSetAttribute(k_deltap_apply<true, false, true, kBT>,
-                             cudaFuncAttributePreferredSharedMemoryCarveout, a);
-        cudaFuncSetAttribute(k_deltap_apply<true, false, false, kBT>,
-                             cudaFuncAttributePreferredSharedMemoryCarveout, a);
-    }
-    void configure_carveouts() {
-        carveout_bt<128>();
-        carveout_bt<256>();
-        cudaGetLastError();
-    }
-
-    template <bool kZ, bool kC>
-    void launch_tile_pair_t(int it, int s, const float4* Pc, float4* Pn, const StateSet& dst,
-                            const SolverConsts& sc, int tslot) {
         cudaStream_t st = ws.stream;
         Ctl* ctl = ws.ctl.p;
-        const int smemL = kCandMax * (int)(sizeof(float4) + sizeof(float));
-        const int smemD = kCandMax * (int)sizeof(float4);
-        KL(k_lambda_tile<kC><<<numTilesP, kTileP, smemL, st>>>(n, it, ctl, tileInfo.p, tileRuns.p,
-                                                                tileMax.p, Pc, dst.W, dst.L, dst.LV,
-                                                                lists16.p, fbLists.p, nbrCount.p,
-                                                                coef16.p, sc, s));
+        const int sb = blocks(n_iter, kLambdaThreads);
+        constexpr int B = kLambdaThreads, K = kBatch;
+        // inverse-mass specialisations (w_mode, checked at upload)
+        if (w_mode == 2)
+            KL(k_lambda<B, K, kZ, 2><<<sb, B, 0, st>>>(n_iter, it, ctl, activeCount.p, order.p, Pc, dst.W, dst.L,
+                                                      nbr.p, nbrCount.p, groupBase.p, sc, s, ownB_, ownE_, PL.p));
+        else if (w_mode == 1)
+            KL(k_lambda<B, K, kZ, 1><<<sb, B, 0, st>>>(n_iter, it, ctl, activeCount.p, order.p, Pc, dst.W, dst.L,
+                                                      nbr.p, nbrCount.p, groupBase.p, sc, s, ownB_, ownE_, PL.p));
+        else
+            KL(k_lambda<B, K, kZ, 0><<<sb, B, 0, st>>>(n_iter, it, ctl, activeCount.p, order.p, Pc, dst.W, dst.L,
+                                                      nbr.p, nbrCount.p, groupBase.p, sc, s, ownB_, ownE_, PL.p));
         if (tslot >= 0) rec(kt_ev[tslot][1]);
-        KL(k_deltap_tile<kZ, kC><<<numTilesP, kTileP, smemD, st>>>(
-            n, it, ctl, tileInfo.p, tileRuns.p, tileMax.p, Pc, Pn, dst.W, dst.L, dst.LV, lists16.p,
-            fbLists.p, nbrCount.p, coef16.p, ws.scene.p, sc, s));
+        constexpr int D = kDeltapThreads;
+        KL(k_deltap_apply<kZ, D, K><<<blocks(n_iter, D), D, 0, st>>>(
+            n_iter, it, ctl, activeCount.p, order.p, Pc, Pn, dst.W, dst.L, dst.LV, nbr.p, nbrCount.p,
+            groupBase.p, ws.scene.p, sc, s, ownB_, ownE_, PL.p));
+    }
+
+    // The list build and the residual pass.
+    void launch_build_lists(int nn, const StateSet& dst) {
+        cudaStream_t st = ws.stream;
+        if (packed_lists)
+            KL(k_build_lists<<<blocks(nn, kListThreads), kListThreads, 0, st>>>(
+                nn, ws.ctl.p, order.p, dst.XS, ws.cellCount.p, cfg.h, cfg.h * cfg.h, nbr.p, nbrCount.p,
+                groupBase.p, nbrCap));
+        else
+            KL(k_build_lists_direct<<<blocks(nn, kListThreads), kListThreads, 0, st>>>(
+                nn, ws.ctl.p, order.p, dst.XS, ws.cellCount.p, cfg.h, cfg.h * cfg.h, nbr.p, nbrCount.p,
+                groupBase.p, list_stride));
+    }
+    void launch_residual(int nn, int it, const float4* Pn, const SolverConsts& sc, double* out, int oB,
+                         int oE) {
+        KL(k_residual<<<blocks(nn, 256), 256, 0, ws.stream>>>(nn, it, ws.ctl.p, activeCount.p, order.p, Pn,
+                                                              nbr.p, nbrCount.p, groupBase.p, sc, out, oB, oE));
+    }
+
+    // The gather passes want L1, not shared memory (they use none).
+    void configure_carveouts() {
+        const int a = cudaSharedmemCarveoutMaxL1;
+        constexpr int B = kLambdaThreads, D = kDeltapThreads, K = kBatch;
+        cudaFuncSetAttribute(k_lambda<B, K, false, 0>, cudaFuncAttributePreferredSharedMemoryCarveout, a);
+        cudaFuncSetAttribute(k_lambda<B, K, false, 1>, cudaFuncAttributePreferredSharedMemoryCarveout, a);
+        cudaFuncSetAttribute(k_lambda<B, K, false, 2>, cudaFuncAttributePreferredSharedMemoryCarveout, a);
+        cudaFuncSetAttribute(k_lambda<B, K, true, 0>, cudaFuncAttributePreferredSharedMemoryCarveout, a);
+        cudaFuncSetAttribute(k_lambda<B, K, true, 1>, cudaFuncAttributePreferredSharedMemoryCarveout, a);
+        cudaFuncSetAttribute(k_lambda<B, K, true, 2>, cudaFuncAttributePreferredSharedMemoryCarveout, a);
+        cudaFuncSetAttribute(k_deltap_apply<false, D, K>, cudaFuncAttributePreferredSharedMemoryCarveout, a);
+        cudaFuncSetAttribute(k_deltap_apply<true, D, K>, cudaFuncAttributePreferredSharedMemoryCarveout, a);
+        // level tables in shared memory: (n_max + 1) ints per CTA, 9x that in
+        // the stable level scatter -- past the 48 KB default from n_max 1365
+        const int lvl = (kMaxLevels + 1) * (int)sizeof(int);
+        CK(cudaFuncSetAttribute(k_level_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, 9 * lvl));
+        CK(cudaFuncSetAttribute(k_gather, cudaFuncAttributeMaxDynamicSharedMemorySize, lvl));
+        CK(cudaFuncSetAttribute(k_level_tiles, cudaFuncAttributeMaxDynamicSharedMemorySize, lvl));
+        cudaGetLastError();
     }
 
     void launch_solver_pair(int it, int s, const float4* Pc, float4* Pn, const StateSet& dst,
                             const SolverConsts& sc, int tslot) {
-        if (use_tiles && !transport) {
-            const int v = (cfg.inactive_lambda_zero ? 2 : 0) | (use_coef ? 1 : 0);
-            switch (v) {
-                case 0: launch_tile_pair_t<false, false>(it, s, Pc, Pn, dst, sc, tslot); break;
-                case 1: launch_tile_pair_t<false, true>(it, s, Pc, Pn, dst, sc, tslot); break;
-                case 2: launch_tile_pair_t<true, false>(it, s, Pc, Pn, dst, sc, tslot); break;
-                default: launch_tile_pair_t<true, true>(it, s, Pc, Pn, dst, sc, tslot); break;
-            }
-            return;
-        }
-        if (use_c16) {
-            const int v = (cfg.inactive_lambda_zero ? 2 : 0) | (use_coef ? 1 : 0);
-            switch (v) {
-                case 0: launch_pair_c16_t<false, false>(it, s, Pc, Pn, dst, sc, tslot); break;
-                case 1: launch_pair_c16_t<false, true>(it, s, Pc, Pn, dst, sc, tslot); break;
-                case 2: launch_pair_c16_t<true, false>(it, s, Pc, Pn, dst, sc, tslot); break;
-                default: launch_pair_c16_t<true, true>(it, s, Pc, Pn, dst, sc, tslot); break;
-            }
-            return;
-        }
-        const int v = (cfg.inactive_lambda_zero ? 4 : 0) | (use_stage ? 2 : 0) | (use_coef ? 1 : 0);
-        switch (v) {
-            case 0: launch_pair_t<false, false, false>(it, s, Pc, Pn, dst, sc, tslot); break;
-            case 1: launch_pair_t<false, false, true>(it, s, Pc, Pn, dst, sc, tslot); break;
-            case 2: launch_pair_t<false, true, false>(it, s, Pc, Pn, dst, sc, tslot); break;
-            case 3: launch_pair_t<false, true, true>(it, s, Pc, Pn, dst, sc, tslot); break;
-            case 4: launch_pair_t<true, false, false>(it, s, Pc, Pn, dst, sc, tslot); break;
-            case 5: launch_pair_t<true, false, true>(it, s, Pc, Pn, dst, sc, tslot); break;
-            case 6: launch_pair_t<true, true, false>(it, s, Pc, Pn, dst, sc, tslot); break;
-            default: launch_pair_t<true, true, true>(it, s, Pc, Pn, dst, sc, tslot); break;
-        }
+        if (cfg.inactive_lambda_zero) launch_pair_t<true>(it, s, Pc, Pn, dst, sc, tslot);
+        else launch_pair_t<false>(it, s, Pc, Pn, dst, sc, tslot);
     }
 
-    // (Re)allocate the order-based list store at nbrCap entries: compact
-    // 16-bit entries, or 32-bit entries plus the coefficient cache.
+    // (Re)allocate the order-based list store at nbrCap entries.
     void alloc_lists() {
         nbr.release();
-        coef.release();
-        nbr16.release();
-        if (use_c16) nbr16.ensure((size_t)nbrCap);
-        else nbr.ensure((size_t)nbrCap);
-        if (use_coef) coef.ensure((size_t)nbrCap);  // only the cache variant reads it
+        nbr.ensure((size_t)nbrCap);
     }
 
-    // After an overflowed list build: leave the compact encoding when its
-    // offsets ran out of range (bit 2), grow whichever store ran out (bit 1).
+    // After an overflowed list build: grow the per-lane stride, or switch to
+    // per-warp slabs when a few lists are very long, or grow the packed store.
     void grow_lists(unsigned long long used, unsigned long long used_fb) {
         const int why = ws.h_ctl->list_overflow;
-        if (!use_tiles) {
-            if (why & 2) use_c16 = false;
-            const bool packed = use_c16 || staged_lists;  // slabs sized per warp by an allocator
-            if ((why & 1) && packed) nbrCap = std::max<long long>(nbrCap * 2, (long long)(used * 3 / 2));
-            if ((why & 1) && !packed) {
-                const int want = std::max(list_stride + 16, (int)used_fb + 8);
-                if (want > kMaxListStride) {
-                    // a few very long lists: a uniform stride would cost n x max;
-                    // switch to per-warp slabs from the allocating builder
-                    staged_lists = true;
-                    nbrCap = std::max<long long>(nbrCap, (long long)(used * 3 / 2));
-                } else {
-                    list_stride = want;
-                }
+        if ((why & 1) && packed_lists) nbrCap = std::max<long long>(nbrCap * 2, (long long)(used * 3 / 2));
+        if ((why & 1) && !packed_lists) {
+            const int want = std::max(list_stride + 16, (int)used_fb + 8);
+            if (want > kMaxListStride) {
+                // a few very long lists: a uniform stride would cost n x max;
+                // switch to per-warp slabs from the allocating builder
+                packed_lists = true;
+                nbrCap = std::max<long long>(nbrCap, (long long)(used * 3 / 2));
+            } else {
+                list_stride = want;
             }
-            if (!use_c16 && !staged_lists) nbrCap = std::max(nbrCap, list_groups * list_stride * 32);
-            alloc_lists();
-            return;
         }
-        if (used > (unsigned long long)listCap16) {
-            listCap16 = std::max<long long>(listCap16 * 2, (long long)(used * 3 / 2));
-            lists16.release();
-            lists16.ensure((size_t)listCap16);
-            coef16.release();
-            coef16.ensure((size_t)listCap16);
-        }
-        if (used_fb > (unsigned long long)fbCap) {
-            fbCap = std::max<long long>(fbCap * 2, (long long)(used_fb * 3 / 2));
-            fbLists.release();
-            fbLists.ensure((size_t)fbCap);
-        }
+        if (!packed_lists) nbrCap = std::max(nbrCap, list_groups * list_stride * 32);
+        alloc_lists();
     }
 
     // Event records that also work inside stream capture (graph event nodes).
@@ -941,32 +754,17 @@ struct apbf_gpu_solver {
                 else CK(cudaStreamWaitEvent(st, ev_inputs, 0));
             }
             KL(k_gather<<<numTiles, kTileThreads, smemG, st>>>(n, ctl, ws.perm.p, pin, dst, nMax, numTiles,
-                                                           tileCount.p, wsort_on() ? cntA.p : nullptr,
-                                                           wsort_on() ? cntB.p : nullptr));
+                                                           tileCount.p));
             if (s == cfg.substeps - 1) rec(ev[7]);  // final storage order (overlapped download)
             KL(k_level_scan<<<nMax + 1, 1024, 0, st>>>(ctl, numTiles, tileCount.p, levelCount.p));
             KL(k_level_finish<<<1, 32, 0, st>>>(ctl, n, nMax, levelCount.p, activeCount.p, bucketStart.p));
-            if (use_tiles && !transport) {
-                KL(k_tile_build<<<numTilesP, kTileP, 0, st>>>(n, ctl, dst.XS, ws.cellCount.p, dst.LV, cfg.h,
-                                                            cfg.h * cfg.h, tileInfo.p, tileRuns.p, tileMax.p,
-                                                            lists16.p, listCap16, fbLists.p, fbCap,
-                                                            nbrCount.p));
-                if (S > 1)
-                    KL(k_prestabilize_slots<<<blocks(n, 256), 256, 0, st>>>(
-                        n, ctl, S, dst.LV, dst.XS, dst.X, ws.scene.p, radius, cfg.stab_iterations, s));
-            } else {
-                KL(k_level_scatter<<<numTiles, kTileThreads, 9 * smemG, st>>>(
-                    n, ctl, dst.LV, nMax, numTiles, tileCount.p, bucketStart.p,
-                    wsort_on() ? orderPre.p : order.p));
-                if (wsort_on())
-                    KL(k_order_window_sort<<<blocks(n, kWSort), kWSort, 0, st>>>(
-                        n, ctl, orderPre.p, order.p, dstpos.p, dst.LV, cntB.p));
-                launch_build_lists(n, dst);
-                if (S > 1)
-                    KL(k_prestabilize<<<blocks(n, 256), 256, 0, st>>>(n, ctl, activeCount.p, S, order.p,
-                                                                   dst.XS, dst.X, ws.scene.p, radius,
-                                                                   cfg.stab_iterations, s));
-            }
+            KL(k_level_scatter<<<numTiles, kTileThreads, 9 * smemG, st>>>(n, ctl, dst.LV, nMax, numTiles,
+                                                                         tileCount.p, bucketStart.p, order.p));
+            launch_build_lists(n, dst);
+            if (S > 1)
+                KL(k_prestabilize<<<blocks(n, 256), 256, 0, st>>>(n, ctl, activeCount.p, S, order.p, dst.XS,
+                                                               dst.X, ws.scene.p, radius, cfg.stab_iterations,
+                                                               s));
             LAUNCH_CHECK();
             mark(2);
             float4* P[2] = {dst.XS, PB.p};
@@ -995,12 +793,7 @@ struct apbf_gpu_solver {
                 if (tslot >= 0) rec(kt_ev[tslot][2]);
                 if (cfg.record_residuals) {
                     CK(cudaMemsetAsync(resid.p + (size_t)s * nMax + (it - 1), 0, sizeof(double), st));
-                    if (use_tiles)
-                        KL(k_residual_tile<<<numTilesP, kTileP, 0, st>>>(
-                            n, it, ctl, activeCount.p, tileInfo.p, tileRuns.p, Pn, lists16.p, fbLists.p,
-                            nbrCount.p, sc, resid.p + (size_t)s * nMax + (it - 1)));
-                    else
-                        launch_residual(n, it, Pn, sc, resid.p + (size_t)s * nMax + (it - 1), 0, 0x7fffffff);
+                    launch_residual(n, it, Pn, sc, resid.p + (size_t)s * nMax + (it - 1), 0, 0x7fffffff);
                 }
                 LAUNCH_CHECK();
                 if (observer) {
@@ -1061,6 +854,11 @@ struct apbf_gpu_solver {
         int32_t* level;
         bool queued;
     };
+    // The caller's x*, lambda and level as passed in (stepFrame overwrites
+    // them before reading them, so the frame never needs them): uploaded raw
+    // on copy_stream while the frame runs, so that a failing frame can hand
+    // the caller back exactly the arrays it passed (restore_host_inputs).
+    DBuf<float> keep;
     HostOut* host_out = nullptr;
     cudaStream_t copy_stream = nullptr;
     cudaEvent_t ev_x = nullptr, ev_inputs = nullptr;  // upload_split: x unpacked / everything unpacked
@@ -1070,7 +868,9 @@ struct apbf_gpu_solver {
     // needs only x), v, mass and inverse mass on copy_stream, unpacked there
     // once x is; the frame waits for ev_vm before its first predict and for
     // ev_inputs before its first reorder.
-    void upload_split(int nn, const float* x, const float* v, const float* mass, const float* inv_mass) {
+    void upload_split(int nn, const float* x, const float* v, const float* mass, const float* inv_mass,
+                      const float* x_star = nullptr, const float* lambda = nullptr,
+                      const int32_t* level = nullptr) {
         n = nn;
         levels_valid = nn == 0;
         if (nn == 0) return;
@@ -1092,6 +892,12 @@ struct apbf_gpu_solver {
         KL(k_unpack_w<<<blocks(nn, 256), 256, 0, copy_stream>>>(nn, d, set[0].view()));
         LAUNCH_CHECK();
         CK(cudaEventRecord(ev_inputs, copy_stream));
+        if (x_star && lambda && level) {  // nothing waits on these (restore_host_inputs only)
+            keep.ensure(5 * (size_t)nn);
+            CK(cudaMemcpyAsync(keep.p, x_star, n3, cudaMemcpyHostToDevice, copy_stream));
+            CK(cudaMemcpyAsync(keep.p + 3LL * nn, lambda, n1, cudaMemcpyHostToDevice, copy_stream));
+            CK(cudaMemcpyAsync(keep.p + 4LL * nn, level, n1, cudaMemcpyHostToDevice, copy_stream));
+        }
         w_agreed = false;
         // The inverse-mass mode picks the lambda variant, so it is part of the
         // frame graph's key.  Scanning 4 B/particle on the host would delay the
@@ -1125,6 +931,31 @@ struct apbf_gpu_solver {
         if (o.xs) CK(cudaMemcpyAsync(o.xs, d + 3LL * n, n3, cudaMemcpyDeviceToHost, st));
         if (o.v) CK(cudaMemcpyAsync(o.v, d + 6LL * n, n3, cudaMemcpyDeviceToHost, st));
         if (o.lambda) CK(cudaMemcpyAsync(o.lambda, d + 11LL * n, n1, cudaMemcpyDeviceToHost, st));
+    }
+
+    // A frame that failed after its overlapped download was queued: give the
+    // caller back the arrays it passed in.  x, v, mass and inverse mass come
+    // from the frame's start set (a single-rank frame never writes those
+    // fields of it), x*, lambda and level from the raw copy of the inputs.
+    void restore_host_inputs(int start) {
+        HostOut& o = *host_out;
+        cudaStream_t st = ws.stream;
+        const StateSet s0 = set[start].view();
+        float* d = stage.p;
+        const size_t n1 = sizeof(float) * (size_t)n, n3 = 3 * n1;
+        CK(cudaStreamSynchronize(copy_stream));
+        KL(k_pack_static<<<blocks(n, 256), 256, 0, st>>>(n, s0, d));
+        KL(k_pack_dynamic<<<blocks(n, 256), 256, 0, st>>>(n, s0, d));
+        LAUNCH_CHECK();
+        CK(cudaMemcpyAsync(o.x, d, n3, cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(o.v, d + 6LL * n, n3, cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(o.mass, d + 9LL * n, n1, cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(o.inv_mass, d + 10LL * n, n1, cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(o.xs, keep.p, n3, cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(o.lambda, keep.p + 3LL * n, n1, cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(o.level, keep.p + 4LL * n, n1, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        o.queued = false;
     }
 
     // Wait for the enqueued frame (and its overlapped download, if any).
@@ -1176,14 +1007,10 @@ struct apbf_gpu_solver {
         k.ktime = kernel_timing;
         k.ptime = phase_timing;
         k.n = n;
-        k.flags = (use_tiles ? 1 : 0) | (use_stage ? 2 : 0) | (use_coef ? 4 : 0) | (use_c16 ? 8 : 0) |
-                  (w_mode << 20) | (staged_lists ? 0x400000 : 0) | (use_wsort ? 0x800000 : 0) | (chunk << 4) |
-                  (block_threads << 8);
+        k.flags = (w_mode << 20) | (packed_lists ? 0x400000 : 0);
         k.caps[0] = nbrCap;
         k.stride = list_stride;
         if (w_mode == 2) std::memcpy(&k.w0bits, &w0, sizeof w0);
-        k.caps[1] = listCap16;
-        k.caps[2] = fbCap;
         if (assign_lod && cam) k.cam = *cam;
         if (assign_lod && lod) k.lod = *lod;
         return k;
@@ -1321,6 +1148,15 @@ struct apbf_gpu_solver {
         if (kernel_timing) collect_kernel_timing(c.total_iterations);
         last_list_entries = c.list_entries;
         last_list_alloc = c.list_alloc;
+        if (c.abort || c.runtime_error) {
+            // A failed frame leaves the state it started from (the reference
+            // throws mid-frame; here the caller gets the frame-start state,
+            // with the frame's LOD levels on the device as assignLevels
+            // wrote them, solver.hpp:247-258), and a host stepFrame's arrays
+            // exactly as they were passed in.
+            cur = start_set;
+            if (host_out && host_out->queued) restore_host_inputs(start_set);
+        }
         if (c.runtime_error) fail(APBF_ERR_RUNTIME, "grid cell count exceeds limit; domain blew up");
         static const char* names[kNumPassSlots] = {"predict", "prestabilize", "lambda",
                                                    "apply",   "finalize",     "finalize"};
@@ -1428,7 +1264,7 @@ struct apbf_gpu_solver {
 
     std::vector<long long> all_counts(Transport& T, long long mine) {
         std::vector<long long> snd(T.size(), mine), rcv(T.size());
-        T.alltoall_counts(snd.data(), rcv.data());
+        T.alltoall_counts(snd.data(), rcv.data(), ws.stream);
         rcv[T.rank()] = mine;
         return rcv;
     }
@@ -1632,7 +1468,7 @@ struct apbf_gpu_solver {
             expand_by_dest(n, G, sendCnt, sendStart);
             const long long nsend = sendStart[G - 1] + sendCnt[G - 1];
             KL(k_pack_recs<<<blocks(nsend, 256), 256, 0, st>>>((int)nsend, sendIdx.p, src, sendRec.p));
-            T.alltoall_counts(sendCnt.data(), recvCnt.data());
+            T.alltoall_counts(sendCnt.data(), recvCnt.data(), st);
             recvCnt[g] = sendCnt[g];
             std::vector<long long> roff(G);
             long long nLocal = 0;
@@ -1795,7 +1631,7 @@ struct apbf_gpu_solver {
         expand_by_dest(n, G, sendCnt, sendStart);
         const long long nsend = sendStart[G - 1] + sendCnt[G - 1];
         KL(k_pack_pm<<<blocks(nsend, 256), 256, 0, st>>>((int)nsend, sendIdx.p, cs.X, cs.XS, sendPM.p));
-        T.alltoall_counts(sendCnt.data(), recvCnt.data());
+        T.alltoall_counts(sendCnt.data(), recvCnt.data(), st);
         recvCnt[g] = sendCnt[g];
         std::vector<long long> roff(G);
         long long nM = 0;
@@ -1956,7 +1792,7 @@ static void validate_config(const apbf_solver_config* c) {
     if (!finite3h(c->gravity)) fail(APBF_ERR_INVALID_ARGUMENT, "gravity must be finite");
     if (c->mode != APBF_MODE_PBF && c->mode != APBF_MODE_APBF)
         fail(APBF_ERR_INVALID_ARGUMENT, "unknown solver mode");
-    if (c->n_max > 4096) fail(APBF_ERR_INVALID_ARGUMENT, "n_max above the GPU level-table limit (4096)");
+    if (c->n_max > kMaxLevels) fail(APBF_ERR_INVALID_ARGUMENT, "n_max above the GPU level-table limit (4096)");
 }
 
 int32_t apbf_gpu_solver_create(const apbf_solver_config* cfg, const apbf_sdf_primitive* prims,
@@ -2042,7 +1878,7 @@ int32_t apbf_gpu_step_frame_host(apbf_gpu_solver* s, int32_t n, float* x, float*
             CK(cudaEventCreate(&t1));
             CK(cudaEventRecord(t0, s->ws.stream));
         }
-        s->upload_split(n, x, v, mass, inv_mass);
+        s->upload_split(n, x, v, mass, inv_mass, x_star, lambda, level);
         auto h1 = std::chrono::steady_clock::now();
         apbf_gpu_solver::HostOut o{x, x_star, v, mass, inv_mass, lambda, level, false};
         s->host_out = &o;
@@ -2271,51 +2107,39 @@ int32_t apbf_gpu_neighbor_lists(int32_t n, const float* positions, float h, floa
         Workspace& ws = component_ws();
         upload_pos4(ws, n, positions);
         component_grid(ws, 0, n, h, padding);
-        // sorted points (the grid's points_ copy), then the cell-tile lists
-        // exactly as the solver builds them (apbf_tiles.cuh), decoded to CSR
+        // sorted points (the grid's points_ copy), then the solver's own list
+        // builder over the identity order (lists by slot), read back as CSR
         cudaStream_t st = ws.stream;
-        const int tiles = (n + kTileP - 1) / kTileP;
+        const int groups = (n + 31) / 32 + 1;
         DBuf<float4> sorted;
-        DBuf<TileInfo> info;
-        DBuf<int2> runs;
-        DBuf<int> tmax, lv, cnt, fb;
-        DBuf<unsigned short> l16;
+        DBuf<int> iota, cnt, lists;
+        DBuf<long long> gbase;
         sorted.ensure(n);
-        info.ensure(tiles);
-        runs.ensure((size_t)tiles * kMaxRuns);
-        tmax.ensure(tiles);
-        lv.ensure(n);
-        cnt.ensure(n);
+        iota.ensure(n);
+        cnt.ensure((size_t)groups * 32);
+        gbase.ensure(groups);
         KL(k_gather_posmass<<<blocks(n, 256), 256, 0, st>>>(n, ws.ctl.p, ws.perm.p, ws.tmp4.p, ws.tmp4.p,
                                                          sorted.p));
-        CK(cudaMemsetAsync(lv.p, 0, sizeof(int) * n, st));
-        long long cap = (long long)tiles * kTileP * 48, fbcap = 4096;
+        KL(k_iota<<<blocks(n, 256), 256, 0, st>>>(iota.p, n));
+        long long cap = (long long)groups * 32 * 48;
         for (;;) {
-            l16.release();
-            l16.ensure((size_t)cap);
-            fb.release();
-            fb.ensure((size_t)fbcap);
+            lists.release();
+            lists.ensure((size_t)cap);
             KL(k_frame_begin<<<1, 1, 0, st>>>(ws.ctl.p));
             KL(k_list_reset<<<1, 1, 0, st>>>(ws.ctl.p));
-            KL(k_tile_build<<<tiles, kTileP, 0, st>>>(n, ws.ctl.p, sorted.p, ws.cellCount.p, lv.p, h, h * h,
-                                                    info.p, runs.p, tmax.p, l16.p, cap, fb.p, fbcap, cnt.p));
+            KL(k_build_lists<<<blocks(n, kListThreads), kListThreads, 0, st>>>(
+                n, ws.ctl.p, iota.p, sorted.p, ws.cellCount.p, h, h * h, lists.p, cnt.p, gbase.p, cap));
             LAUNCH_CHECK();
             ws.read_ctl();
             if (!ws.h_ctl->list_overflow) break;
             cap = std::max<long long>(cap * 2, (long long)ws.h_ctl->list_alloc * 3 / 2);
-            fbcap = std::max<long long>(fbcap * 2, (long long)ws.h_ctl->list_alloc_fb * 3 / 2);
         }
-        std::vector<int> hc(n);
-        std::vector<TileInfo> hi(tiles);
-        std::vector<int2> hr((size_t)tiles * kMaxRuns);
-        const long long used = (long long)ws.h_ctl->list_alloc, usedfb = (long long)ws.h_ctl->list_alloc_fb;
-        std::vector<unsigned short> h16((size_t)std::max<long long>(used, 1));
-        std::vector<int> hfb((size_t)std::max<long long>(usedfb, 1));
+        const long long used = (long long)ws.h_ctl->list_alloc;
+        std::vector<int> hc(n), hl((size_t)std::max<long long>(used, 1));
+        std::vector<long long> hb(groups);
         CK(cudaMemcpy(hc.data(), cnt.p, sizeof(int) * n, cudaMemcpyDeviceToHost));
-        CK(cudaMemcpy(hi.data(), info.p, sizeof(TileInfo) * tiles, cudaMemcpyDeviceToHost));
-        CK(cudaMemcpy(hr.data(), runs.p, sizeof(int2) * hr.size(), cudaMemcpyDeviceToHost));
-        if (used > 0) CK(cudaMemcpy(h16.data(), l16.p, sizeof(unsigned short) * used, cudaMemcpyDeviceToHost));
-        if (usedfb > 0) CK(cudaMemcpy(hfb.data(), fb.p, sizeof(int) * usedfb, cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(hb.data(), gbase.p, sizeof(long long) * groups, cudaMemcpyDeviceToHost));
+        if (used > 0) CK(cudaMemcpy(hl.data(), lists.p, sizeof(int) * used, cudaMemcpyDeviceToHost));
         long long total = 0;
         for (int i = 0; i < n; ++i) total += hc[i];
         if (total_out) *total_out = total;
@@ -2327,20 +2151,8 @@ int32_t apbf_gpu_neighbor_lists(int32_t n, const float* positions, float h, floa
             if (indices_capacity < total) fail(APBF_ERR_INVALID_ARGUMENT, "indices capacity too small");
             long long w = 0;
             for (int i = 0; i < n; ++i) {
-                const int t = i / kTileP, p = i % kTileP;
-                const TileInfo& ti = hi[t];
-                const long long off = (long long)ti.listBase + (long long)p * ti.cap;
-                for (int e = 0; e < hc[i]; ++e) {
-                    if (ti.C < 0) {
-                        indices[w++] = hfb[off + e];
-                    } else {
-                        const int c = h16[off + e];
-                        int r = 0;
-                        while (r + 1 < ti.nRuns && hr[(size_t)t * kMaxRuns + r + 1].y <= c) ++r;
-                        const int2 run = hr[(size_t)t * kMaxRuns + r];
-                        indices[w++] = run.x + (c - run.y);
-                    }
-                }
+                const long long b0 = hb[i >> 5] + (i & 31);
+                for (int e = 0; e < hc[i]; ++e) indices[w++] = hl[b0 + (long long)e * 32];
             }
         }
     });
@@ -2366,6 +2178,69 @@ int32_t apbf_gpu_all_densities(int32_t n, const float* positions, const float* m
         LAUNCH_CHECK();
         CK(cudaMemcpyAsync(rho_out, rho.p, sizeof(float) * n, cudaMemcpyDeviceToHost, st));
         CK(cudaStreamSynchronize(st));
+    });
+}
+
+// The vorticity estimate of the opt-in post-pass (apbf_post.cuh, eq. 15 of
+// Macklin & Mueller 2013) for arbitrary positions/velocities: the same grid,
+// lists and k_post_omega the solver runs, omega in input index order.
+int32_t apbf_gpu_vorticity(int32_t n, const float* positions, const float* velocities, float h,
+                           float* omega_out, apbf_error* err) {
+    return guarded(err, [&] {
+        if (n == 0) return;
+        check_grid_args(n, positions, h, h);
+        if (!velocities || !omega_out) fail(APBF_ERR_INVALID_ARGUMENT, "null velocities or output");
+        Workspace& ws = component_ws();
+        upload_pos4(ws, n, positions);
+        component_grid(ws, 0, n, h, h);
+        cudaStream_t st = ws.stream;
+        const int groups = (n + 31) / 32 + 1;
+        DBuf<float4> sorted, vin, vs, om, vx;
+        DBuf<int> iota, cnt, lists;
+        DBuf<long long> gbase;
+        DBuf<float> stage;
+        sorted.ensure(n);
+        vin.ensure(n);
+        vs.ensure(n);
+        om.ensure(n);
+        vx.ensure(n);
+        iota.ensure(n);
+        cnt.ensure((size_t)groups * 32);
+        gbase.ensure(groups);
+        stage.ensure(3 * (size_t)n);
+        CK(cudaMemcpyAsync(stage.p, velocities, sizeof(float) * 3 * n, cudaMemcpyHostToDevice, st));
+        KL(k_unpack_x<<<blocks(n, 256), 256, 0, st>>>(n, stage.p, vin.p));
+        KL(k_gather_posmass<<<blocks(n, 256), 256, 0, st>>>(n, ws.ctl.p, ws.perm.p, ws.tmp4.p, ws.tmp4.p,
+                                                         sorted.p));
+        KL(k_gather_posmass<<<blocks(n, 256), 256, 0, st>>>(n, ws.ctl.p, ws.perm.p, vin.p, vin.p, vs.p));
+        KL(k_iota<<<blocks(n, 256), 256, 0, st>>>(iota.p, n));
+        long long cap = (long long)groups * 32 * 48;
+        for (;;) {
+            lists.release();
+            lists.ensure((size_t)cap);
+            KL(k_frame_begin<<<1, 1, 0, st>>>(ws.ctl.p));
+            KL(k_list_reset<<<1, 1, 0, st>>>(ws.ctl.p));
+            KL(k_build_lists<<<blocks(n, kListThreads), kListThreads, 0, st>>>(
+                n, ws.ctl.p, iota.p, sorted.p, ws.cellCount.p, h, h * h, lists.p, cnt.p, gbase.p, cap));
+            LAUNCH_CHECK();
+            ws.read_ctl();
+            if (!ws.h_ctl->list_overflow) break;
+            cap = std::max<long long>(cap * 2, (long long)ws.h_ctl->list_alloc * 3 / 2);
+        }
+        KL(k_post_omega<<<blocks(n, 256), 256, 0, st>>>(n, ws.ctl.p, iota.p, sorted.p, vs.p, lists.p, cnt.p,
+                                                     gbase.p, make_kernel_consts(h), 0.0f, om.p, vx.p));
+        LAUNCH_CHECK();
+        std::vector<float4> ho(n);
+        std::vector<int> perm(n);
+        CK(cudaMemcpyAsync(ho.data(), om.p, sizeof(float4) * n, cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(perm.data(), ws.perm.p, sizeof(int) * n, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        for (int k = 0; k < n; ++k) {
+            float* o = omega_out + 3LL * perm[k];
+            o[0] = ho[k].x;
+            o[1] = ho[k].y;
+            o[2] = ho[k].z;
+        }
     });
 }
 

@@ -3,10 +3,15 @@
 // substep's finalize.  The reference has neither, so
 // they are OFF by default (xsph_c = vorticity_eps = 0 leaves every frame
 // bit-identical to the reference) and sit outside the parity contract; the
-// tests check them against a float64 restatement of the same discretisation.
+// tests check them against an independent float64 implementation of the
+// paper's equations and against analytic fields (rigid rotation: omega =
+// +2 Omega z).
 //
-//   omega_i = sum_j (v_j - v_i) x gradW(x_i - x_j)                 (eq. 15)
-//   eta_i   = sum_j (|omega_j| - |omega_i|) gradW(x_i - x_j)
+// gradW(x_i - x_j) below is the spiky gradient with respect to x_i
+// (spiky_grad).  Eq. 15 differentiates with respect to p_j, which is its
+// negative, so the SPH curl estimate reads
+//   omega_i = sum_j (v_i - v_j) x gradW(x_i - x_j)                 (eq. 15)
+//   eta_i   = sum_j (|omega_j| - |omega_i|) gradW(x_i - x_j)      (grad |omega|)
 //   N_i     = eta_i / |eta_i|  (0 when eta_i = 0)
 //   v_i    += dt * eps * (N_i x omega_i)                          (eq. 16)
 //   v_i    += c * sum_j (v_j - v_i) W(x_i - x_j)                  (eq. 17, XSPH)
@@ -43,9 +48,10 @@ __global__ void k_post_omega(int n, const Ctl* ctl, const int* __restrict__ orde
         float gx, gy, gz;
         spiky_grad(kc, r2, rx, ry, rz, gx, gy, gz);
         const float ux = vj.x - vi.x, uy = vj.y - vi.y, uz = vj.z - vi.z;
-        ox += uy * gz - uz * gy;
-        oy += uz * gx - ux * gz;
-        oz += ux * gy - uy * gx;
+        // (v_i - v_j) x g = -(u x g) = g x u
+        ox += gy * uz - gz * uy;
+        oy += gz * ux - gx * uz;
+        oz += gx * uy - gy * ux;
         const float w = poly6_r2(kc, r2);
         sx += ux * w;
         sy += uy * w;

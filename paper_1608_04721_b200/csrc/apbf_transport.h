@@ -41,8 +41,9 @@ struct Transport {
     // are ignored (the caller copies locally).
     virtual void alltoallv(const void* const* send, const size_t* sendBytes, void* const* recv,
                            const size_t* recvBytes, cudaStream_t st) = 0;
-    // Host all-to-all of one int64 per destination.
-    virtual void alltoall_counts(const long long* send, long long* recv) = 0;
+    // Host all-to-all of one int64 per destination, ordered on `st` (returns
+    // once recv is filled: the solver stream is synchronised).
+    virtual void alltoall_counts(const long long* send, long long* recv, cudaStream_t st) = 0;
 };
 
 template <class T>
@@ -149,7 +150,7 @@ struct LoopbackTransport final : Transport {
         hub->barrier();  // senders may reuse their buffers now
     }
 
-    void alltoall_counts(const long long* send, long long* recv) override {
+    void alltoall_counts(const long long* send, long long* recv, cudaStream_t) override {
         hub->counts[r_].assign(send, send + hub->G);
         hub->barrier();
         for (int q = 0; q < hub->G; ++q) recv[q] = hub->counts[q][r_];
@@ -254,21 +255,25 @@ struct NcclTransport final : Transport {
         }
         check(api.groupEnd(), "ncclGroupEnd");
     }
-    void alltoall_counts(const long long* send, long long* recv) override {
-        // scratch layout: [0, g) send, [g, 2g) recv
+    void alltoall_counts(const long long* send, long long* recv, cudaStream_t st) override {
+        // scratch layout: [0, g) send, [g, 2g) recv; all on the solver stream
         long long* d = (long long*)scratch;
-        cudaMemcpy(d, send, sizeof(long long) * g_, cudaMemcpyHostToDevice);
+        cuda_check(cudaMemcpyAsync(d, send, sizeof(long long) * g_, cudaMemcpyHostToDevice, st), "counts upload");
         NcclApi& api = NcclApi::get();
         check(api.groupStart(), "ncclGroupStart");
         for (int q = 0; q < g_; ++q) {
             if (q == r_) continue;
-            check(api.send(d + q, 8, 0, q, comm, 0), "ncclSend");
-            check(api.recv(d + g_ + q, 8, 0, q, comm, 0), "ncclRecv");
+            check(api.send(d + q, 8, 0, q, comm, st), "ncclSend");
+            check(api.recv(d + g_ + q, 8, 0, q, comm, st), "ncclRecv");
         }
         check(api.groupEnd(), "ncclGroupEnd");
-        cudaDeviceSynchronize();
-        cudaMemcpy(recv, d + g_, sizeof(long long) * g_, cudaMemcpyDeviceToHost);
+        cuda_check(cudaMemcpyAsync(recv, d + g_, sizeof(long long) * g_, cudaMemcpyDeviceToHost, st),
+                   "counts download");
+        cuda_check(cudaStreamSynchronize(st), "counts exchange");
         recv[r_] = send[r_];
+    }
+    static void cuda_check(cudaError_t e, const char* what) {
+        if (e != cudaSuccess) throw std::runtime_error(std::string(what) + ": " + cudaGetErrorString(e));
     }
 };
 

@@ -20,6 +20,8 @@ def clouds():
         "collinear": np.array([[0, 0, 0], [0.05, 0, 0], [0.1, 0, 0]], np.float32),
         "singleton": np.array([[0.3, -0.2, 0.1]], np.float32),
         "coincident": np.zeros((17, 3), np.float32),
+        # ~100 members per h=0.05 cell: the heavy-cell sort (k_heavy_sort)
+        "dense_cells": rng.uniform(0.0, 0.1, (1200, 3)).astype(np.float32),
     }
     for name, scale in (("dam_break", 15625 / 216000), ("double_dam_break", 0.05),
                         ("multi_dam_break", 0.1)):
@@ -41,6 +43,27 @@ def test_grid_build_bitwise(name, h):
     assert np.array_equal(g.dims, dims)
     assert np.array_equal(g.cell_start, cs)
     assert np.array_equal(g.perm, perm)
+
+
+@pytest.mark.parametrize("n,cells", [(200_000, 1), (300_000, 3), (150_000, 40)])
+def test_grid_build_collapsed_cloud_is_linear_and_bitwise(n, cells):
+    """A collapsed cloud (the reference allows it) puts 10^5 particles into a
+    few cells.  The stable in-cell order must still equal the reference's
+    serial counting sort (uniform_grid.hpp:83-94), without the O(occupancy^2)
+    cost of ranking by comparisons: the whole build stays well under a second."""
+    import time
+    rng = np.random.default_rng(n)
+    centers = rng.uniform(0.0, 1.0, (cells, 3)).astype(np.float32)
+    p = centers[rng.integers(0, cells, n)] + rng.uniform(0, 1e-4, (n, 3)).astype(np.float32)
+    p = p.astype(np.float32)
+    grid_build(p[:1000], 0.05, 0.05)  # warm up the workspace
+    t0 = time.perf_counter()
+    g = grid_build(p, 0.05, 0.05)
+    dt = time.perf_counter() - t0
+    perm, origin, dims, cs = O.oracle_grid_build(p, 0.05, 0.05)
+    assert np.array_equal(g.cell_start, cs)
+    assert np.array_equal(g.perm, perm)
+    assert dt < 1.0, dt
 
 
 @pytest.mark.parametrize("name", sorted(CLOUDS))

@@ -380,3 +380,72 @@ def test_state_set_rotation_and_graph_cache_bitwise(substeps):
         orc.step_frame(b, spec.camera, spec.lod, f)
     for k in ("x", "x_star", "v", "mass", "inv_mass", "lambda_", "level"):
         assert np.array_equal(getattr(a, k), getattr(b, k)), k
+
+
+FIELDS7 = ("x", "x_star", "v", "mass", "inv_mass", "lambda_", "level")
+
+
+@pytest.mark.parametrize("fault", ["nan_velocity", "blow_up"])
+def test_failed_frame_leaves_caller_arrays_untouched(fault):
+    """A frame that fails (NumericalError in predict, or the grid's cell-count
+    guard) must not hand the caller a half-written state: the host stepFrame
+    downloads overlap the frame, so a failure restores exactly the arrays the
+    caller passed in -- in the eager first frame and in a replayed graph --
+    and the solver carries on from its start state afterwards."""
+    spec = S.build_scenario("dam_break", 4096 / 216000)
+    spec.solver.range = IterationRange(3, 6)
+    sv = Solver(spec.solver, spec.scene)
+    orc = O.OracleSolver(spec.solver, spec.scene)
+    good = S.make_state(spec, 2)
+    ref = good.copy()
+    for f in range(4):  # eager, capture, replay ...
+        bad = good.copy()
+        bad.x_star[:] = np.float32(7.0)  # not read by stepFrame, but must come back as passed
+        bad.lambda_[:] = np.float32(-3.0)
+        bad.level[:] = 4
+        if fault == "nan_velocity":
+            bad.v[123, 1] = np.nan
+            exc = NumericalError
+        else:
+            bad.v[77, 0] = np.float32(1.25e8)  # x* 1e5 m away: > 2^26 grid cells
+            exc = RuntimeError
+        before = bad.copy()
+        with pytest.raises(exc):
+            sv.step_frame(bad, spec.camera, spec.lod, f)
+        for k in FIELDS7:
+            assert np.array_equal(getattr(bad, k), getattr(before, k), equal_nan=True), (f, k)
+        sv.step_frame(good, spec.camera, spec.lod, f)
+        orc.step_frame(ref, spec.camera, spec.lod, f)
+        for k in FIELDS7:
+            assert np.array_equal(getattr(good, k), getattr(ref, k)), (f, k)
+
+
+def test_failed_resident_frame_keeps_start_state():
+    """Resident frames: after a failure the device state is the frame-start
+    state (step_frame_with_levels downloads it unchanged)."""
+    spec = S.build_scenario("dam_break", 4096 / 216000)
+    spec.solver.range = IterationRange(3, 6)
+    st = S.make_state(spec, 3)
+    st.level[:] = 5
+    st.v[11, 0] = np.inf
+    before = st.copy()
+    sv = Solver(spec.solver, spec.scene)
+    with pytest.raises(NumericalError):
+        sv.step_frame_with_levels(st, 0)
+    for k in FIELDS7:
+        assert np.array_equal(getattr(st, k), getattr(before, k), equal_nan=True), k
+
+
+def test_large_iteration_range_runs_like_oracle():
+    """n_max past 1365 needs more than the 48 KB default of shared memory for
+    the level tables (9 * (n_max + 1) ints in the stable level scatter): the
+    kernels opt into the larger limit, so every n_max the config accepts runs."""
+    x = lattice(4, 0.04, (0.2, 0.2, 0.2))
+    c = cfg_(h=0.1, substeps=1, range=IterationRange(1500, 2000), mode=SolverMode.PBF)
+    a = ParticleSet(x, 0.064, 2000)
+    b = a.copy()
+    sa = Solver(c).step_frame_with_levels(a, 0)
+    sb = O.OracleSolver(c).step_frame_with_levels(b, 0)
+    assert sa.total_iterations == sb.total_iterations == 64 * 2000
+    for k in FIELDS7:
+        assert np.array_equal(getattr(a, k), getattr(b, k)), k
