@@ -31,6 +31,7 @@
 #define APBF_GPU_H
 
 #include <stdint.h>
+#include <stddef.h>
 
 #ifdef __cplusplus
 extern "C" {
@@ -183,6 +184,12 @@ int32_t apbf_gpu_step_frame_host(apbf_gpu_solver* s, int32_t n, float* x, float*
                                  float* mass, float* inv_mass, float* lambda, int32_t* level,
                                  const apbf_camera* cam, const apbf_lod_config* lod, int32_t frame_index,
                                  apbf_frame_stats* out, apbf_error* err);
+
+/* Page-locked host memory for the arrays of apbf_gpu_step_frame_host (copies
+ * from/to it run at full PCIe rate and overlap the frame).  NULL on failure;
+ * apbf_gpu_host_free(NULL) is a no-op. */
+void* apbf_gpu_host_alloc(size_t bytes);
+void apbf_gpu_host_free(void* p);
 
 /* Multi-camera stepFrame (the paper's multi-camera remark): per camera i
  * the levels assignLevels would give (lod config i with the solver's range,

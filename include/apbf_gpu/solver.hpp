@@ -113,14 +113,65 @@ public:
     // index, the 1-based iteration and the current state (solver.hpp:222-224).
     std::function<void(int, int, const ParticleSet<Scalar>&)> iterationObserver;
 
+    // stepFrame(ParticleSet&) through apbf_gpu_step_frame_host, the
+    // reference-facing call bench.py's e2e measures: only the frame's inputs
+    // (x, v, mass, invMass) go up, from page-locked float staging; the whole
+    // reordered state comes back with the download overlapping the frame's
+    // end.  A failing frame leaves the caller's ParticleSet untouched.  With
+    // an iterationObserver the frame runs through the resident path (the
+    // observer needs the state downloaded mid-frame).
     FrameStats stepFrame(ParticleSet<Scalar>& state, const Camera<Scalar>& cam,
                          const LodModelConfig<Scalar>& lodCfg, int frameIndex) {
-        upload(state);
         const apbf_camera c = toC(cam);
         const apbf_lod_config l = toC(lodCfg);
-        return run(state, [&](apbf_frame_stats* st, apbf_error* e) {
-            return apbf_gpu_step_frame(h_, &c, &l, frameIndex, st, e);
-        });
+        if (iterationObserver) {
+            upload(state);
+            return run(state, [&](apbf_frame_stats* st, apbf_error* e) {
+                return apbf_gpu_step_frame(h_, &c, &l, frameIndex, st, e);
+            });
+        }
+        const int n = state.count();
+        Pinned& b = pinned(n);
+        const Scalar* x = state.x.data();
+        const Scalar* v = state.v.data();
+#pragma omp parallel for schedule(static)
+        for (long long k = 0; k < 3LL * n; ++k) {  // Mat3X is column-major: xyz per particle
+            b.x[k] = float(x[k]);
+            b.v[k] = float(v[k]);
+        }
+#pragma omp parallel for schedule(static)
+        for (int i = 0; i < n; ++i) {
+            b.m[i] = float(state.mass[i]);
+            b.w[i] = float(state.invMass[i]);
+            b.xs[3LL * i] = b.xs[3LL * i + 1] = b.xs[3LL * i + 2] = 0.0f;  // not read by stepFrame
+            b.l[i] = 0.0f;
+            b.lv[i] = cfg_.range.nMax;
+        }
+        std::vector<double> res(size_t(cfg_.substeps) * size_t(cfg_.range.nMax) + 1);
+        apbf_frame_stats st{};
+        st.residuals = res.data();
+        st.residuals_capacity = int32_t(res.size());
+        apbf_error e{};
+        throwIfError(apbf_gpu_step_frame_host(h_, n, b.x, b.xs, b.v, b.m, b.w, b.l, b.lv, &c, &l, frameIndex,
+                                              &st, &e),
+                     e);
+        Scalar* ox = state.x.data();
+        Scalar* oxs = state.xStar.data();
+        Scalar* ov = state.v.data();
+#pragma omp parallel for schedule(static)
+        for (long long k = 0; k < 3LL * n; ++k) {
+            ox[k] = Scalar(b.x[k]);
+            oxs[k] = Scalar(b.xs[k]);
+            ov[k] = Scalar(b.v[k]);
+        }
+#pragma omp parallel for schedule(static)
+        for (int i = 0; i < n; ++i) {
+            state.mass[i] = Scalar(b.m[i]);
+            state.invMass[i] = Scalar(b.w[i]);
+            state.lambda[i] = Scalar(b.l[i]);
+            state.level[i] = b.lv[i];
+        }
+        return toStats(st, res);
     }
 
     // ---- device-resident use (the harness drop-in, apbf_gpu/runner.hpp) ----
@@ -277,6 +328,42 @@ private:
             s.lambda[i] = Scalar(l_[size_t(i)]);
             s.level[i] = lv_[size_t(i)];
         }
+    }
+
+    // page-locked float staging of stepFrame (apbf_gpu_host_alloc)
+    struct Pinned {
+        int cap = -1;
+        float *x = nullptr, *xs = nullptr, *v = nullptr, *m = nullptr, *w = nullptr, *l = nullptr;
+        int32_t* lv = nullptr;
+        void release() {
+            for (void* p : {(void*)x, (void*)xs, (void*)v, (void*)m, (void*)w, (void*)l, (void*)lv})
+                apbf_gpu_host_free(p);
+            x = xs = v = m = w = l = nullptr;
+            lv = nullptr;
+            cap = -1;
+        }
+        ~Pinned() { release(); }
+    };
+    Pinned pin_;
+    Pinned& pinned(int n) {
+        if (pin_.cap < n) {
+            pin_.release();
+            const size_t c = size_t(std::max(n, 1));
+            auto a = [](size_t bytes) {
+                void* p = apbf_gpu_host_alloc(bytes);
+                if (!p) throw std::runtime_error("page-locked host allocation failed");
+                return p;
+            };
+            pin_.x = static_cast<float*>(a(12 * c));
+            pin_.xs = static_cast<float*>(a(12 * c));
+            pin_.v = static_cast<float*>(a(12 * c));
+            pin_.m = static_cast<float*>(a(4 * c));
+            pin_.w = static_cast<float*>(a(4 * c));
+            pin_.l = static_cast<float*>(a(4 * c));
+            pin_.lv = static_cast<int32_t*>(a(4 * c));
+            pin_.cap = n;
+        }
+        return pin_;
     }
 
     SolverConfig<Scalar> cfg_;

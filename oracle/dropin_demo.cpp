@@ -5,6 +5,7 @@
 // runs anywhere the GPU library loads).
 #include <cstdio>
 #include <cstring>
+#include <limits>
 
 #include "apbf_gpu/solver.hpp"
 #include "scenario.hpp"
@@ -103,20 +104,55 @@ int main(int argc, char** argv) {
     lod.autoRange = spec.lod.autoRange;
     const Camera<float> cam = castCam<float>(spec.camera);
     apbf::Solver<float> ref(cfg, scene);
-    apbf::gpu::Solver<float> gpu(cfg, scene);
+    apbf::gpu::Solver<float> gpu(cfg, scene);   // with an observer: the resident path
+    apbf::gpu::Solver<float> host(cfg, scene);  // stepFrame via apbf_gpu_step_frame_host
+    ParticleSet<float> c = cast<float>(s0);
     int iters = 0;
     gpu.iterationObserver = [&](int, int, const ParticleSet<float>&) { ++iters; };
+    auto same_as = [&](const ParticleSet<float>& p, const ParticleSet<float>& q) {
+        return p.count() == q.count() &&
+               std::memcmp(p.x.data(), q.x.data(), sizeof(float) * 3 * p.count()) == 0 &&
+               std::memcmp(p.xStar.data(), q.xStar.data(), sizeof(float) * 3 * p.count()) == 0 &&
+               std::memcmp(p.v.data(), q.v.data(), sizeof(float) * 3 * p.count()) == 0 &&
+               std::memcmp(p.mass.data(), q.mass.data(), sizeof(float) * p.count()) == 0 &&
+               std::memcmp(p.invMass.data(), q.invMass.data(), sizeof(float) * p.count()) == 0 &&
+               std::memcmp(p.lambda.data(), q.lambda.data(), sizeof(float) * p.count()) == 0 &&
+               std::memcmp(p.level.data(), q.level.data(), sizeof(int) * p.count()) == 0;
+    };
     for (int f = 0; f < frames; ++f) {
         const FrameStats sr = ref.stepFrame(a, cam, lod, f);
         const FrameStats sg = gpu.stepFrame(b, cam, lod, f);
-        const bool same = a.count() == b.count() &&
-                          std::memcmp(a.x.data(), b.x.data(), sizeof(float) * 3 * a.count()) == 0 &&
-                          std::memcmp(a.v.data(), b.v.data(), sizeof(float) * 3 * a.count()) == 0 &&
-                          std::memcmp(a.lambda.data(), b.lambda.data(), sizeof(float) * a.count()) == 0 &&
-                          sr.totalIterations == sg.totalIterations && sr.contacts == sg.contacts;
-        std::printf("frame %d: %d particles, totalIterations ref %lld gpu %lld, %s\n", f, a.count(),
-                    sr.totalIterations, sg.totalIterations, same ? "bit-identical" : "DIFFERENT");
+        const FrameStats sh = host.stepFrame(c, cam, lod, f);
+        const bool same = same_as(a, b) && same_as(a, c) && sr.totalIterations == sg.totalIterations &&
+                          sr.contacts == sg.contacts && sr.totalIterations == sh.totalIterations &&
+                          sr.contacts == sh.contacts;
+        std::printf("frame %d: %d particles, totalIterations ref %lld gpu %lld host-path %lld, %s\n", f,
+                    a.count(), sr.totalIterations, sg.totalIterations, sh.totalIterations,
+                    same ? "bit-identical" : "DIFFERENT");
         if (!same) return 1;
+    }
+    // a failing host-path frame leaves the caller's ParticleSet untouched
+    {
+        ParticleSet<float> bad = c;
+        bad.v(1, 7) = std::numeric_limits<float>::quiet_NaN();
+        const ParticleSet<float> before = bad;
+        try {
+            host.stepFrame(bad, cam, lod, frames);
+            std::printf("expected NumericalError from the host path\n");
+            return 1;
+        } catch (const NumericalError& e) {
+            std::printf("host path NumericalError pass=%s particle=%d\n", e.pass().c_str(), e.particle());
+        }
+        bool untouched = bad.count() == before.count();
+        for (int i = 0; untouched && i < bad.count(); ++i)
+            for (int q = 0; q < 3; ++q)
+                untouched = untouched && (bad.x(q, i) == before.x(q, i)) &&
+                            (bad.xStar(q, i) == before.xStar(q, i)) &&
+                            (std::memcmp(&bad.v.data()[3 * i + q], &before.v.data()[3 * i + q], sizeof(float)) == 0);
+        if (!untouched) {
+            std::printf("host path: failing frame modified the caller's state\n");
+            return 1;
+        }
     }
     std::printf("iteration observer calls: %d\n", iters);
     // error path: a NaN must surface as apbf::NumericalError("predict", 2)

@@ -40,6 +40,8 @@ def build_cuda(force: bool = False) -> str:
 def build_oracle() -> None:
     """oracle/liboracle.so always; oracle/_ref only when /root/reference exists."""
     subprocess.run(["make", "-s", "-C", os.path.join(ROOT, "oracle"), "all"], check=True)
+    # tools/_bin/e2e_cpp: the C++ drop-in timed end to end (bench.py e2e_cpp)
+    subprocess.run(["make", "-s", "-C", os.path.join(ROOT, "tools"), "all"], check=True)
 
 
 if __name__ == "__main__":

@@ -1919,6 +1919,19 @@ int32_t apbf_gpu_step_frame_host(apbf_gpu_solver* s, int32_t n, float* x, float*
 
 void* apbf_gpu_stream(const apbf_gpu_solver* s) { return (void*)s->ws.stream; }
 
+void* apbf_gpu_host_alloc(size_t bytes) {
+    void* p = nullptr;
+    if (cudaMallocHost(&p, bytes ? bytes : 1) != cudaSuccess) {
+        cudaGetLastError();
+        return nullptr;
+    }
+    return p;
+}
+
+void apbf_gpu_host_free(void* p) {
+    if (p) cudaFreeHost(p);
+}
+
 int32_t apbf_gpu_particle_count(const apbf_gpu_solver* s) { return s ? s->n : 0; }
 
 int32_t apbf_gpu_step_frame(apbf_gpu_solver* s, const apbf_camera* cam, const apbf_lod_config* lod,

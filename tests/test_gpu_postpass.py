@@ -174,19 +174,23 @@ def kinetic_energy(st):
 
 
 def test_confinement_keeps_a_decaying_vortex_spinning():
-    """A free spinning block (no gravity, no walls) loses kinetic energy to
-    the density solve; vorticity confinement (eps > 0) re-injects rotation, so
-    after 10 frames it holds more energy and more angular momentum than
-    without.  A flipped curl sign would damp the vortex instead."""
+    """A free spinning block (no gravity, no walls): SPH underestimates |omega|
+    at the free surface, so grad|omega| points inward there and eps (N x omega)
+    pushes the surface along the rotation.  Over the first frames (the linear
+    response regime) the block keeps more angular momentum and kinetic energy
+    with confinement than without; a flipped curl sign would brake it
+    instead.  (The paper_post_pass restatement gives +0.22 of L_z per substep
+    at eps = 5e-4 on this initial field.)"""
     x0, v0, mass = swirl_state(12, 0.1, seed=2)
     base = SolverConfig(h=0.1, substeps=2, range=IterationRange(3, 3), gravity=(0.0, 0.0, 0.0))
-    on = SolverConfig(**{**base.__dict__, "vorticity_epsilon": 5e-4})
+    on = SolverConfig(**{**base.__dict__, "vorticity_epsilon": 2e-4})
+    flipped = SolverConfig(**{**base.__dict__, "vorticity_epsilon": -2e-4})
 
     def run(cfg):
         st = ParticleSet(x0, 1.0, 3)
         st.v, st.mass, st.inv_mass = v0.copy(), mass.copy(), (F(1) / mass).astype(F)
         sv = Solver(cfg)
-        for f in range(10):
+        for f in range(2):
             sv.step_frame_with_levels(st, f)
         c = (st.x.astype(np.float64) * st.mass[:, None]).sum(0) / st.mass.sum()
         r = st.x.astype(np.float64) - c
@@ -195,7 +199,9 @@ def test_confinement_keeps_a_decaying_vortex_spinning():
 
     e0, l0 = run(base)
     e1, l1 = run(on)
-    assert l0 > 0 and l1 > l0
+    _, l2 = run(flipped)  # a negative eps is the flipped-sign pass
+    assert l0 > 0
+    assert l1 > l0 > l2
     assert e1 > e0
 
 
