@@ -18,10 +18,11 @@ e2e    = the same metric through the reference-facing call with HOST buffers:
          cores) on the same workload.
 
 Usage: python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-N > 1 is launched by torchrun (one process per GPU): the C3 ocean extended N
-times along z (1M particles per GPU, weak scaling) runs as ONE domain,
+N > 1 is launched by torchrun (one process per GPU): C5, the fixed 8M-particle
+tank (scenarios/tank_8m.cfg, BASELINE.json configs[4]) runs as ONE domain,
 z-slab decomposed with NCCL migration/halo exchanges (paper_1608_04721_b200/
-slab.py); every FrameStats total is global.
+slab.py), strong scaling; rank 0 also times the same 8M tank alone on its
+GPU (t1) so the line carries t1/tN.  Every FrameStats total is global.
 """
 from __future__ import annotations
 
@@ -56,6 +57,7 @@ def parse():
     ap.add_argument("--seed", type=int, default=1)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-fast", action="store_true", help="skip the fast-build (FMA) twin measurement")
     ap.add_argument("--cpu-frames", type=int, default=1, help="timed reference frames (cpu_baseline)")
     return ap.parse_args()
 
@@ -137,10 +139,29 @@ def ncu_kernel(kernel: str):
         return None, None
 
 
-def cpu_reference_sample(spec, seed, frames):
+def bench_scenario(args, world):
+    """C3 (1M ocean) on one GPU; C5 (8M tank, strong scaling) on N > 1."""
+    return args.scenario if world == 1 else "tank_8m"
+
+
+def make_config(spec, world, args):
+    """The `config` object of the JSON line -- identical in both arms."""
+    n = spec.particle_count()
+    return {"workload": f"{spec.name}: {n} particles, APBF {spec.solver.range.n_min}..{spec.solver.range.n_max}, "
+                        f"lod={spec.lod.model.name.lower()}, {spec.solver.substeps} substeps, "
+                        "metrics pass included",
+            "scenario_file": f"scenarios/{spec.name}.cfg", "seed": args.seed,
+            "parallelism": "single GPU" if world == 1 else
+            f"{world} z-slabs (strong scaling of the fixed {n}-particle domain), NCCL migration+halo "
+            "all-to-all per substep, x* halo per iteration",
+            "l2": "inputs larger than L2 (~0.5 GB device state + scratch per frame)"}
+
+
+def cpu_reference_sample(spec, seed, frames, warmup=1, prec=8):
     """The reference CPU implementation on a bounded sample of the workload:
-    `frames` full stepFrame calls of the same scenario (after one warm-up
-    frame), Solver<double> over all host cores (deterministic=false)."""
+    `frames` full stepFrame calls of the same scenario (after `warmup`
+    warm-up frames), Solver<double> (prec 8, as shipped) or Solver<float>
+    (prec 4) over all host cores (deterministic=false)."""
     import numpy as np
 
     from oracle import oracle as O
@@ -153,23 +174,83 @@ def cpu_reference_sample(spec, seed, frames):
                         np.zeros(n), np.full(n, spec.solver.range.n_max, np.int32))
         cfg = spec.solver
         cfg.deterministic = False
-        sv = O.RefSolver(cfg, spec.scene, prec=8)
+        sv = O.RefSolver(cfg, spec.scene, prec=prec)
         kind, cores = "reference", int(O.rlib().ref_omp_threads())
     else:
         st = S.make_state(spec, seed)
         sv = O.OracleSolver(spec.solver, spec.scene)
-        kind, cores = "port", 1
-    sv.step_frame(st, spec.camera, spec.lod, 0)
+        kind, cores, prec = "port", 1, 4
+    for f in range(warmup):
+        sv.step_frame(st, spec.camera, spec.lod, f)
     t0 = time.perf_counter()
     its = 0
     for f in range(frames):
-        its += sv.step_frame(st, spec.camera, spec.lod, 1 + f).total_iterations
+        its += sv.step_frame(st, spec.camera, spec.lod, warmup + f).total_iterations
     dt = time.perf_counter() - t0
+    what = (f"Solver<{'double' if prec == 8 else 'float'}> from /root/reference via oracle/_ref"
+            if kind == "reference" else "C oracle port (float)")
     return {"value": its / dt, "unit": UNIT, "cores": cores, "kind": kind,
             "sample": f"{frames} full stepFrame(s) of {spec.name} ({spec.particle_count()} particles, "
-                      f"APBF {{{spec.solver.range.n_min}..{spec.solver.range.n_max}}}) after 1 warm-up "
-                      f"frame; {'Solver<double> from /root/reference via oracle/_ref' if kind == 'reference' else 'C oracle port'}",
+                      f"APBF {{{spec.solver.range.n_min}..{spec.solver.range.n_max}}}) after {warmup} warm-up "
+                      f"frame(s); {what}",
             "seconds_per_step": dt / frames}
+
+
+def rooflines(kt, ms_kt, nbar, sm_mhz, hbm_peak, peak_kind, steps, fma):
+    """HBM (algorithmic bytes) and FP32 rooflines of the dominant solver pass
+    from the per-launch CUDA-event times of an instrumented region."""
+    dom = "deltap_apply" if kt["deltap_ms"] >= kt["lambda_ms"] else "lambda"
+    dom_ms = kt["deltap_ms"] if dom == "deltap_apply" else kt["lambda_ms"]
+    per_launch_ms = dom_ms / max(1, kt["launches"])
+    pis_per_launch = kt["particle_iterations"] / max(1, kt["launches"])
+    alg_bytes = BYTES_PER_PI[dom] * pis_per_launch
+    achieved = alg_bytes / (per_launch_ms / 1e3) / 1e9
+    flops_pi = {"lambda": 37 * (nbar - 1) + 31, "deltap_apply": 23 * (nbar - 1) + 7}[dom]
+    traffic, t_ncu = ncu_kernel(f"k_{dom}" + ("_fast" if fma else ""))
+    traffic_gbs = traffic / t_ncu / 1e9 if traffic and t_ncu else None  # measured DRAM bytes / s
+    fp32_peak = 148 * 128 * sm_mhz * 1e6 / 1e12 * (2 if fma else 1)
+    fp32_achieved = flops_pi * pis_per_launch / (per_launch_ms / 1e3) / 1e12
+    roof = {"bound": "hbm", "kernel": f"k_{dom}", "achieved": achieved,
+            "peak": hbm_peak, "unit": "GB/s", "frac": achieved / hbm_peak,
+            "peak_source": peak_kind, "traffic": traffic,
+            "traffic_gbs_ncu": traffic_gbs,
+            "traffic_frac_ncu": traffic_gbs / hbm_peak if traffic_gbs else None,
+            "traffic_over_algorithmic": traffic / alg_bytes if traffic else None,
+            "algorithmic_bytes_per_launch": alg_bytes,
+            "avg_launch_ms": per_launch_ms, "launches": kt["launches"],
+            "share_of_step": dom_ms / ms_kt,
+            "share_of_step_both_passes": (kt["lambda_ms"] + kt["deltap_ms"]) / ms_kt,
+            "timing": f"CUDA events around every solver-pass launch on the solver stream, "
+                      f"over a twin region of the same {steps} frames",
+            "note": "gather/latency-bound kernel; the ALGORITHMIC-byte HBM fraction is low by "
+                    "construction (SURVEY.md 8d: list scratch excluded); "
+                    "traffic_*_ncu = the measured DRAM bytes of one full launch over its "
+                    "ncu duration; see also roofline_fp32"}
+    roof32 = {"bound": "fp32", "achieved": fp32_achieved, "peak": fp32_peak,
+              "unit": "TFLOP/s", "frac": fp32_achieved / fp32_peak, "nbar": nbar,
+              "flops_per_particle_iteration": flops_pi,
+              "peak_note": "148 SMs x 128 lanes x median SM clock" + (" x 2 (FMA)" if fma else ", no FMA credit")}
+    return roof, roof32
+
+
+def e2e_cpp(args):
+    """The C++ drop-in a reference maintainer would add (apbf::gpu::Solver<double>
+    ::stepFrame over the reference's own ParticleSet<double>, scenario loader
+    and types; tools/_bin/e2e_cpp), timed end to end per stepFrame call."""
+    exe = os.path.join(ROOT, "tools", "_bin", "e2e_cpp")
+    if not os.access(exe, os.X_OK):
+        return {"unavailable": "tools/_bin/e2e_cpp not built (needs /root/reference at build time)"}
+    try:
+        out = subprocess.run([exe, os.path.join(ROOT, "scenarios", f"{args.scenario}.cfg"), str(args.steps),
+                              "3", "f64"], capture_output=True, text=True, timeout=600)
+        r = json.loads(out.stdout.strip().splitlines()[-1])
+    except Exception as e:  # report, do not fail the bench line
+        return {"unavailable": f"e2e_cpp failed: {e}"}
+    return {"value": r["particle_iterations_per_s"], "unit": UNIT, "ms_per_step": r["ms_per_step"],
+            "median_ms": r["median_ms"], "binding": r["binding"], "frames": r["frames"],
+            "note": "std::chrono around each stepFrame on the caller's ParticleSet<double>: double->float "
+                    "conversion, page-locked staging, upload of the frame's inputs, the frame, the overlapped "
+                    "download and float->double conversion of all 13 words per particle"}
 
 
 def dist_setup(args):
@@ -210,24 +291,27 @@ def allreduce_sum(pg, v: float) -> float:
 
 
 def run_reference(args, world, rank):
+    """The reference's own CPU stepFrame (Solver<double> as shipped, OpenMP
+    over all host cores) on this arm's workload: W warm-up frames, then K
+    timed frames (one full stepFrame each), plus a Solver<float> value on a
+    3-frame sample beside it.  Rank 0 only."""
     if rank != 0:
         return 0
     from paper_1608_04721_b200 import scenario as S
-    spec = S.build_scenario(args.scenario)
-    # bounded: each step is one full frame of the 1M workload on the CPU
-    steps = max(1, min(args.steps, 5))
-    res = cpu_reference_sample(spec, args.seed, steps)
+    spec = S.build_scenario(bench_scenario(args, world))
+    res = cpu_reference_sample(spec, args.seed, args.steps, warmup=args.warmup)
+    f32 = cpu_reference_sample(S.build_scenario(bench_scenario(args, world)), args.seed, 3, warmup=1, prec=4)
     line = {"metric": METRIC, "value": res["value"], "unit": UNIT, "n_gpus": args.gpus,
-            "steps": steps, "warmup": 1, "ms_per_step": res["seconds_per_step"] * 1e3,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic", "impl": "reference",
-            "config": {"workload": f"{spec.name}: {spec.particle_count()} particles, APBF "
-                                   f"{spec.solver.range.n_min}..{spec.solver.range.n_max}, "
-                                   f"lod={spec.lod.model.name.lower()}, rank 0 only",
-                       "scenario_file": f"scenarios/{args.scenario}.cfg", "seed": args.seed},
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": res["seconds_per_step"] * 1e3,
+            "higher_is_better": True, "scaling": "weak" if world == 1 else "strong", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic", "impl": "reference",
+            "config": make_config(spec, world, args),
             "cpu_baseline": {k: res[k] for k in ("value", "unit", "cores", "kind", "sample")},
+            "reference_f32": {k: f32[k] for k in ("value", "unit", "cores", "kind", "sample")},
             "e2e": {"value": res["value"], "unit": UNIT, "h2d_bytes_per_step": 0,
-                    "d2h_bytes_per_step": 0}}
+                    "d2h_bytes_per_step": 0},
+            "note": "the reference's Eigen dependency is absent from the image: it is compiled unmodified "
+                    "against oracle/eigen_min (an eager Eigen-subset shim written here), -O3 -fopenmp"}
     print(json.dumps(line), flush=True)
     return 0
 
@@ -241,10 +325,7 @@ def run_ours(args, world, rank, local, pg):
     from paper_1608_04721_b200.slab import SlabSolver, nccl_unique_id, slice_state
 
     torch.cuda.set_device(local)
-    if world == 1:
-        spec = S.build_scenario(args.scenario)
-    else:
-        spec = S.ocean_weak(world)
+    spec = S.build_scenario(bench_scenario(args, world))
     n_global = spec.particle_count()
     cam, lod = spec.camera, spec.lod
     if world == 1:
@@ -304,8 +385,63 @@ def run_ours(args, world, rank, local, pg):
         kt = solver.kernel_times()
         solver.set_kernel_timing(False)
 
+    # ------- the fast build (apbf_gpu_set_fast_math), same frames, reported beside -------
+    fast = None
+    if world == 1 and not args.no_fast:
+        solver.set_fast_math(True)
+        for f in range(3):
+            solver.step_frame_resident(cam, lod, 1700 + f)
+        torch.cuda.synchronize()
+        e0.record(ext)
+        its_f = 0
+        for f in range(args.steps):
+            its_f += solver.step_frame_resident(cam, lod, 1800 + f).total_iterations
+        e1.record(ext)
+        e1.synchronize()
+        ms_f = e0.elapsed_time(e1)
+        solver.set_kernel_timing(True)
+        for f in range(3):
+            solver.step_frame_resident(cam, lod, 1900 + f)
+        solver.set_kernel_timing(True)
+        torch.cuda.synchronize()
+        e0.record(ext)
+        for f in range(args.steps):
+            solver.step_frame_resident(cam, lod, 2000 + f)
+        e1.record(ext)
+        e1.synchronize()
+        fast = {"value": its_f / (ms_f / 1e3), "unit": UNIT, "ms_per_step": ms_f / args.steps,
+                "kt": solver.kernel_times(), "ms_kt": e0.elapsed_time(e1)}
+        solver.set_kernel_timing(False)
+        solver.set_fast_math(False)
+
     ms_max = allreduce_max(pg, ms)
     value = its / (ms_max / 1e3)  # FrameStats totals are already global
+
+    # ------- N > 1: the same fixed domain on ONE GPU (rank 0), for t1 / tN -------
+    strong = None
+    if world > 1:
+        barrier(pg)
+        if rank == 0:
+            one = Solver(spec.solver, spec.scene, device=local)
+            one.upload(S.make_state(spec, args.seed))
+            ext1 = torch.cuda.ExternalStream(one.stream_handle(), device=local)
+            for f in range(max(3, args.warmup)):
+                one.step_frame_resident(cam, lod, f)
+            torch.cuda.synchronize()
+            e0.record(ext1)
+            its1 = 0
+            for f in range(args.steps):
+                its1 += one.step_frame_resident(cam, lod, 1000 + f).total_iterations
+            e1.record(ext1)
+            e1.synchronize()
+            t1 = e0.elapsed_time(e1) / args.steps
+            strong = {"t1_ms_per_step": t1, "tN_ms_per_step": ms_max / args.steps,
+                      "speedup_t1_over_tN": t1 / (ms_max / args.steps), "n_gpus": world,
+                      "t1_value": its1 / (t1 * args.steps / 1e3),
+                      "note": f"t1: the same {n_global}-particle domain stepped by the plain solver on rank "
+                              f"0's GPU alone, same frames count, after the N-GPU timed region"}
+            del one
+        barrier(pg)
 
     # ---------------- e2e through the C-ABI with host buffers ----------------
     e2e = None
@@ -383,61 +519,42 @@ def run_ours(args, world, rank, local, pg):
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": max(3, args.warmup), "ms_per_step": ms_max / args.steps,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-        "data": "synthetic",
-        "config": {"workload": f"{spec.name}: {n_global} particles ({n_global // world} per GPU), APBF "
-                               f"{spec.solver.range.n_min}..{spec.solver.range.n_max}, "
-                               f"lod={spec.lod.model.name.lower()}, {spec.solver.substeps} substeps, "
-                               "metrics pass included",
-                   "scenario_file": "scenarios/ocean_1m.cfg" + ("" if world == 1 else f" x{world} along z"),
-                   "seed": args.seed,
-                   "parallelism": "single GPU" if world == 1 else
-                   f"{world} z-slabs, NCCL migration+halo all-to-all per substep, x* halo per iteration",
-                   "l2": "inputs larger than L2 (~0.5 GB device state + scratch per frame)"},
+        "higher_is_better": True, "scaling": "weak" if world == 1 else "strong", "vs_baseline": None,
+        "dtype": "f32", "data": "synthetic",
+        "config": make_config(spec, world, args),
         "steps_per_s": args.steps / (ms_max / 1e3),
         "particle_iterations_per_step": its / args.steps,
         "e2e": e2e,
         "gpu_launches": launches,
         "clocks": clk,
     }
+    if strong is not None:
+        line["strong_scaling"] = strong
+    if world == 1 and not args.no_e2e:
+        line["e2e_cpp"] = e2e_cpp(args)
     if world == 1:
-        dom = "deltap_apply" if kt["deltap_ms"] >= kt["lambda_ms"] else "lambda"
-        dom_ms = kt["deltap_ms"] if dom == "deltap_apply" else kt["lambda_ms"]
-        per_launch_ms = dom_ms / max(1, kt["launches"])
-        pis_per_launch = kt["particle_iterations"] / max(1, kt["launches"])
-        alg_bytes = BYTES_PER_PI[dom] * pis_per_launch
-        achieved = alg_bytes / (per_launch_ms / 1e3) / 1e9
-        nbar = entries / n_global
-        flops_pi = {"lambda": 37 * (nbar - 1) + 31, "deltap_apply": 23 * (nbar - 1) + 7}[dom]
-        traffic, t_ncu = ncu_kernel(f"k_{dom}")
-        traffic_gbs = traffic / t_ncu / 1e9 if traffic and t_ncu else None  # measured DRAM bytes / s
         sm_mhz = clk.get("sm_mhz") or 1965.0
-        fp32_peak = 148 * 128 * sm_mhz * 1e6 / 1e12
-        fp32_achieved = flops_pi * pis_per_launch / (per_launch_ms / 1e3) / 1e12
-        line["roofline"] = {"bound": "hbm", "kernel": f"k_{dom}", "achieved": achieved,
-                            "peak": hbm_peak, "unit": "GB/s", "frac": achieved / hbm_peak,
-                            "peak_source": peak_kind, "traffic": traffic,
-                            "traffic_gbs_ncu": traffic_gbs,
-                            "traffic_frac_ncu": traffic_gbs / hbm_peak if traffic_gbs else None,
-                            "algorithmic_bytes_per_launch": alg_bytes,
-                            "avg_launch_ms": per_launch_ms, "launches": kt["launches"],
-                            "share_of_step": dom_ms / ms_kt,
-                            "share_of_step_both_passes": (kt["lambda_ms"] + kt["deltap_ms"]) / ms_kt,
-                            "timing": f"CUDA events around every solver-pass launch on the solver stream, "
-                                      f"over a twin region of the same {args.steps} frames",
-                            "note": "gather/latency-bound kernel; the ALGORITHMIC-byte HBM fraction is low by "
-                                    "construction (SURVEY.md 8d: list/coefficient scratch excluded); "
-                                    "traffic_*_ncu = the measured DRAM bytes of one full launch over its "
-                                    "ncu duration; see also roofline_fp32"}
-        line["roofline_fp32"] = {"bound": "fp32", "achieved": fp32_achieved, "peak": fp32_peak,
-                                 "unit": "TFLOP/s", "frac": fp32_achieved / fp32_peak, "nbar": nbar,
-                                 "flops_per_particle_iteration": flops_pi,
-                                 "peak_note": "148 SMs x 128 lanes x median SM clock, no FMA credit"}
+        line["roofline"], line["roofline_fp32"] = rooflines(kt, ms_kt, entries / n_global, sm_mhz, hbm_peak,
+                                                            peak_kind, args.steps, fma=False)
+        if fast is not None:
+            rf, rf32 = rooflines(fast["kt"], fast["ms_kt"], entries / n_global, sm_mhz, hbm_peak, peak_kind,
+                                 args.steps, fma=True)
+            line["fast_build"] = {
+                "value": fast["value"], "unit": UNIT, "ms_per_step": fast["ms_per_step"],
+                "roofline": rf, "roofline_fp32": rf32,
+                "kernel_ms": {"lambda_total": fast["kt"]["lambda_ms"], "deltap_apply_total": fast["kt"]["deltap_ms"],
+                              "instrumented_region_total": fast["ms_kt"]},
+                "note": "apbf_gpu_set_fast_math(1): FMA-contracted lambda/delta-p pair arithmetic with rsqrt "
+                        "instead of the correctly rounded sqrt and division; outside the bitwise contract, "
+                        "within tier-B tolerance of the reference's Solver<double> (tests/test_gpu_fast_math.py); "
+                        "same workload, timed after the parity-build regions"}
         line["kernel_ms"] = {"lambda_total": kt["lambda_ms"], "deltap_apply_total": kt["deltap_ms"],
                              "instrumented_region_total": ms_kt, "clean_region_total": ms}
         if not args.no_cpu_baseline:
             res = cpu_reference_sample(S.build_scenario(args.scenario), args.seed, args.cpu_frames)
             line["cpu_baseline"] = {k: res[k] for k in ("value", "unit", "cores", "kind", "sample")}
+            f32 = cpu_reference_sample(S.build_scenario(args.scenario), args.seed, args.cpu_frames, prec=4)
+            line["cpu_baseline"]["reference_f32"] = {k: f32[k] for k in ("value", "unit", "cores", "sample")}
     print(json.dumps(line), flush=True)
     return 0
 

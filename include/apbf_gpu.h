@@ -206,6 +206,15 @@ int32_t apbf_gpu_step_frame_multi(apbf_gpu_solver* s, int32_t k, const apbf_came
 typedef void (*apbf_iteration_observer)(void* user, int32_t substep, int32_t iteration);
 int32_t apbf_gpu_set_iteration_observer(apbf_gpu_solver* s, apbf_iteration_observer cb, void* user);
 
+/* Fast build of the lambda and delta-p pair arithmetic (default off):
+ * FMA contraction, |g|^2 = c^2 r^2, and 1/|r| from one rsqrt approximation
+ * instead of the correctly rounded sqrt and division of the reference's
+ * gradientKernel (kernels.hpp:52-65).  Outside the bitwise contract: results
+ * stay within the tier-B tolerance of the reference's Solver<double> (2x its
+ * own float-vs-double divergence, tests/test_gpu_fast_math.py).  Takes effect
+ * at the next frame. */
+int32_t apbf_gpu_set_fast_math(apbf_gpu_solver* s, int32_t enabled);
+
 /* Frame-time switch for the end-of-frame density metrics pass
  * (solver.hpp:271-279); on by default like the reference. */
 int32_t apbf_gpu_set_frame_metrics(apbf_gpu_solver* s, int32_t enabled);

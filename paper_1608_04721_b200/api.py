@@ -544,6 +544,11 @@ class Solver:
         return stats
 
     # --- profiling hooks ---
+    def set_fast_math(self, enabled: bool) -> None:
+        """apbf_gpu_set_fast_math: contracted lambda / delta-p pair arithmetic
+        (outside the bitwise contract; tier-B tolerance)."""
+        self._lib.apbf_gpu_set_fast_math(self._h, int(enabled))
+
     def set_frame_metrics(self, enabled: bool) -> None:
         self._lib.apbf_gpu_set_frame_metrics(self._h, int(enabled))
 

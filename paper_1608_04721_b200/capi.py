@@ -126,6 +126,7 @@ SIGNATURES = {
     "apbf_gpu_all_densities": (C.c_int32, [C.c_int32, _fp, _fp, C.c_float, _fp, _ep]),
     "apbf_gpu_vorticity": (C.c_int32, [C.c_int32, _fp, _fp, C.c_float, _fp, _ep]),
     "apbf_gpu_host_alloc": (C.c_void_p, [C.c_size_t]),
+    "apbf_gpu_set_fast_math": (C.c_int32, [C.c_void_p, C.c_int32]),
     "apbf_gpu_host_free": (None, [C.c_void_p]),
     "apbf_gpu_lod_dtc": (C.c_int32, [C.c_int32, _fp, C.POINTER(apbf_camera),
                                      C.POINTER(apbf_lod_config), _ip, _ep]),

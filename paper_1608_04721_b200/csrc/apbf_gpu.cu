@@ -598,8 +598,11 @@ struct apbf_gpu_solver {
     // 128-thread CTAs, delta-p in 256) and the neighbour gathers in flight
     // per batch.
     static constexpr int kLambdaThreads = 128, kDeltapThreads = 256, kBatch = 4;
+    // apbf_gpu_set_fast_math: the contracted lambda / delta-p pair arithmetic
+    // (fast_pair_coef), outside the bitwise contract
+    bool fast_math = false;
 
-    template <bool kZ>
+    template <bool kZ, bool kF>
     void launch_pair_t(int it, int s, const float4* Pc, float4* Pn, const StateSet& dst,
                        const SolverConsts& sc, int tslot) {
         cudaStream_t st = ws.stream;
@@ -608,17 +611,20 @@ struct apbf_gpu_solver {
         constexpr int B = kLambdaThreads, K = kBatch;
         // inverse-mass specialisations (w_mode, checked at upload)
         if (w_mode == 2)
-            KL(k_lambda<B, K, kZ, 2><<<sb, B, 0, st>>>(n_iter, it, ctl, activeCount.p, order.p, Pc, dst.W, dst.L,
-                                                      nbr.p, nbrCount.p, groupBase.p, sc, s, ownB_, ownE_, PL.p));
+            KL(k_lambda<B, K, kZ, 2, kF><<<sb, B, 0, st>>>(n_iter, it, ctl, activeCount.p, order.p, Pc, dst.W,
+                                                          dst.L, nbr.p, nbrCount.p, groupBase.p, sc, s, ownB_,
+                                                          ownE_, PL.p));
         else if (w_mode == 1)
-            KL(k_lambda<B, K, kZ, 1><<<sb, B, 0, st>>>(n_iter, it, ctl, activeCount.p, order.p, Pc, dst.W, dst.L,
-                                                      nbr.p, nbrCount.p, groupBase.p, sc, s, ownB_, ownE_, PL.p));
+            KL(k_lambda<B, K, kZ, 1, kF><<<sb, B, 0, st>>>(n_iter, it, ctl, activeCount.p, order.p, Pc, dst.W,
+                                                          dst.L, nbr.p, nbrCount.p, groupBase.p, sc, s, ownB_,
+                                                          ownE_, PL.p));
         else
-            KL(k_lambda<B, K, kZ, 0><<<sb, B, 0, st>>>(n_iter, it, ctl, activeCount.p, order.p, Pc, dst.W, dst.L,
-                                                      nbr.p, nbrCount.p, groupBase.p, sc, s, ownB_, ownE_, PL.p));
+            KL(k_lambda<B, K, kZ, 0, kF><<<sb, B, 0, st>>>(n_iter, it, ctl, activeCount.p, order.p, Pc, dst.W,
+                                                          dst.L, nbr.p, nbrCount.p, groupBase.p, sc, s, ownB_,
+                                                          ownE_, PL.p));
         if (tslot >= 0) rec(kt_ev[tslot][1]);
         constexpr int D = kDeltapThreads;
-        KL(k_deltap_apply<kZ, D, K><<<blocks(n_iter, D), D, 0, st>>>(
+        KL(k_deltap_apply<kZ, D, K, kF><<<blocks(n_iter, D), D, 0, st>>>(
             n_iter, it, ctl, activeCount.p, order.p, Pc, Pn, dst.W, dst.L, dst.LV, nbr.p, nbrCount.p,
             groupBase.p, ws.scene.p, sc, s, ownB_, ownE_, PL.p));
     }
@@ -642,17 +648,22 @@ struct apbf_gpu_solver {
     }
 
     // The gather passes want L1, not shared memory (they use none).
-    void configure_carveouts() {
+    template <bool kF>
+    static void carveouts_f() {
         const int a = cudaSharedmemCarveoutMaxL1;
         constexpr int B = kLambdaThreads, D = kDeltapThreads, K = kBatch;
-        cudaFuncSetAttribute(k_lambda<B, K, false, 0>, cudaFuncAttributePreferredSharedMemoryCarveout, a);
-        cudaFuncSetAttribute(k_lambda<B, K, false, 1>, cudaFuncAttributePreferredSharedMemoryCarveout, a);
-        cudaFuncSetAttribute(k_lambda<B, K, false, 2>, cudaFuncAttributePreferredSharedMemoryCarveout, a);
-        cudaFuncSetAttribute(k_lambda<B, K, true, 0>, cudaFuncAttributePreferredSharedMemoryCarveout, a);
-        cudaFuncSetAttribute(k_lambda<B, K, true, 1>, cudaFuncAttributePreferredSharedMemoryCarveout, a);
-        cudaFuncSetAttribute(k_lambda<B, K, true, 2>, cudaFuncAttributePreferredSharedMemoryCarveout, a);
-        cudaFuncSetAttribute(k_deltap_apply<false, D, K>, cudaFuncAttributePreferredSharedMemoryCarveout, a);
-        cudaFuncSetAttribute(k_deltap_apply<true, D, K>, cudaFuncAttributePreferredSharedMemoryCarveout, a);
+        cudaFuncSetAttribute(k_lambda<B, K, false, 0, kF>, cudaFuncAttributePreferredSharedMemoryCarveout, a);
+        cudaFuncSetAttribute(k_lambda<B, K, false, 1, kF>, cudaFuncAttributePreferredSharedMemoryCarveout, a);
+        cudaFuncSetAttribute(k_lambda<B, K, false, 2, kF>, cudaFuncAttributePreferredSharedMemoryCarveout, a);
+        cudaFuncSetAttribute(k_lambda<B, K, true, 0, kF>, cudaFuncAttributePreferredSharedMemoryCarveout, a);
+        cudaFuncSetAttribute(k_lambda<B, K, true, 1, kF>, cudaFuncAttributePreferredSharedMemoryCarveout, a);
+        cudaFuncSetAttribute(k_lambda<B, K, true, 2, kF>, cudaFuncAttributePreferredSharedMemoryCarveout, a);
+        cudaFuncSetAttribute(k_deltap_apply<false, D, K, kF>, cudaFuncAttributePreferredSharedMemoryCarveout, a);
+        cudaFuncSetAttribute(k_deltap_apply<true, D, K, kF>, cudaFuncAttributePreferredSharedMemoryCarveout, a);
+    }
+    void configure_carveouts() {
+        carveouts_f<false>();
+        carveouts_f<true>();
         // level tables in shared memory: (n_max + 1) ints per CTA, 9x that in
         // the stable level scatter -- past the 48 KB default from n_max 1365
         const int lvl = (kMaxLevels + 1) * (int)sizeof(int);
@@ -664,8 +675,13 @@ struct apbf_gpu_solver {
 
     void launch_solver_pair(int it, int s, const float4* Pc, float4* Pn, const StateSet& dst,
                             const SolverConsts& sc, int tslot) {
-        if (cfg.inactive_lambda_zero) launch_pair_t<true>(it, s, Pc, Pn, dst, sc, tslot);
-        else launch_pair_t<false>(it, s, Pc, Pn, dst, sc, tslot);
+        const int v = (cfg.inactive_lambda_zero ? 1 : 0) | (fast_math ? 2 : 0);
+        switch (v) {
+            case 0: launch_pair_t<false, false>(it, s, Pc, Pn, dst, sc, tslot); break;
+            case 1: launch_pair_t<true, false>(it, s, Pc, Pn, dst, sc, tslot); break;
+            case 2: launch_pair_t<false, true>(it, s, Pc, Pn, dst, sc, tslot); break;
+            default: launch_pair_t<true, true>(it, s, Pc, Pn, dst, sc, tslot); break;
+        }
     }
 
     // (Re)allocate the order-based list store at nbrCap entries.
@@ -1007,7 +1023,7 @@ struct apbf_gpu_solver {
         k.ktime = kernel_timing;
         k.ptime = phase_timing;
         k.n = n;
-        k.flags = (w_mode << 20) | (packed_lists ? 0x400000 : 0);
+        k.flags = (w_mode << 20) | (packed_lists ? 0x400000 : 0) | (fast_math ? 1 : 0);
         k.caps[0] = nbrCap;
         k.stride = list_stride;
         if (w_mode == 2) std::memcpy(&k.w0bits, &w0, sizeof w0);
@@ -2012,6 +2028,12 @@ int32_t apbf_gpu_step_frame_with_levels(apbf_gpu_solver* s, int32_t frame_index,
 int32_t apbf_gpu_set_iteration_observer(apbf_gpu_solver* s, apbf_iteration_observer cb, void* user) {
     s->observer = cb;
     s->observer_user = user;
+    return APBF_OK;
+}
+
+int32_t apbf_gpu_set_fast_math(apbf_gpu_solver* s, int32_t enabled) {
+    if (!s) return APBF_ERR_INVALID_ARGUMENT;
+    s->fast_math = enabled != 0;
     return APBF_OK;
 }
 
