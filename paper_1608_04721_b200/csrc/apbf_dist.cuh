@@ -12,6 +12,7 @@
 #pragma once
 
 #include "apbf_kernels.cuh"
+#include "apbf_transport.h"
 
 namespace apbf_gpu {
 
@@ -24,10 +25,20 @@ __device__ __forceinline__ int layer_of(const GridDev& G, float h, float z) {
 
 // Work per cz layer (global grid g) -> hist[dims.z]: each particle counts
 // with its level (its particle-iterations this substep), so equal-sum slabs
-// balance the solver work of APBF rather than the particle count.
+// balance the solver work of APBF rather than the particle count.  The
+// histogram holds `cap` layers (a device-sized grid): a deeper grid flags
+// need_layers and aborts the frame (identically on every rank: the grid is
+// global), and the host grows the histogram and runs the frame again.
 __global__ void k_layer_hist(int n, const float4* __restrict__ P, const int* __restrict__ LV,
-                             const Ctl* ctl, int g, float h, int* __restrict__ hist) {
+                             Ctl* ctl, int g, float h, int* __restrict__ hist, int cap) {
     if (ctl->abort) return;
+    if (ctl->grid[g].dims[2] > cap) {
+        if (blockIdx.x == 0 && threadIdx.x == 0) {
+            ctl->need_layers = ctl->grid[g].dims[2];
+            ctl->abort = 1;
+        }
+        return;
+    }
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     // storage order is cell order, so a warp's particles share few layers:
     // one atomic per distinct layer of the warp (match + reduce), not per particle
@@ -38,17 +49,88 @@ __global__ void k_layer_hist(int n, const float4* __restrict__ P, const int* __r
     if (key >= 0 && (threadIdx.x & 31) == __ffs(same) - 1) atomicAdd(&hist[key], sum);
 }
 
-// Destination bit mask: bit q set when cz in [lo[q] - halo, hi[q] + halo).
+// The slab partition on the device (identical on every rank: same global
+// histogram in, same slabs out), so no host round trip sits between the
+// histogram all-reduce and the exchange.  Too few layers: slab_error + abort.
+__global__ void k_slab_partition(const int* __restrict__ hist, Ctl* ctl, int G, int minLayers,
+                                 int* __restrict__ zr) {
+    if (ctl->abort) return;
+    if (!slab_partition(hist, ctl->grid[0].dims[2], G, minLayers, zr, zr + G)) {
+        ctl->slab_error = 1;
+        ctl->abort = 1;
+    }
+}
+
+// Per-destination record classes of a substep's exchange, sent ahead of the
+// records so that the receiver knows every size of its substep after ONE
+// host synchronisation: [0] total, [1..4] records in layers lo-2 .. lo+1,
+// [5..8] records in layers hi-2 .. hi+1 of the destination's slab [lo, hi).
+// (The receiver's stable cell sort puts them in z-major order, so its slab
+// bounds are prefix sums of these.)
+constexpr int kCls = 9;
+
+// Destination bit mask: bit q set when cz in [lo[q] - halo, hi[q] + halo);
+// with cls != nullptr also the kCls class counts per destination (per-CTA
+// shared-memory counters, one global atomic per non-zero counter and CTA).
 __global__ void k_dest_mask(int n, const float4* __restrict__ P, const Ctl* ctl, int g, float h,
                             const int* __restrict__ lo, const int* __restrict__ hi, int G, int halo,
-                            unsigned* __restrict__ mask) {
+                            unsigned* __restrict__ mask, int* __restrict__ cls = nullptr) {
+    __shared__ int s_cls[kMaxRanks * kCls];
+    if (cls) {
+        for (int t = threadIdx.x; t < G * kCls; t += blockDim.x) s_cls[t] = 0;
+        __syncthreads();
+    }
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    const int cz = layer_of(ctl->grid[g], h, P[i].z);
-    unsigned m = 0;
-    for (int q = 0; q < G; ++q)
-        if (cz >= lo[q] - halo && cz < hi[q] + halo) m |= 1u << q;
-    mask[i] = m;
+    if (i < n && !ctl->abort) {
+        const int cz = layer_of(ctl->grid[g], h, P[i].z);
+        unsigned m = 0;
+        for (int q = 0; q < G; ++q) {
+            const int l = lo[q], u = hi[q];
+            if (cz >= l - halo && cz < u + halo) {
+                m |= 1u << q;
+                if (cls) {
+                    atomicAdd(&s_cls[q * kCls], 1);
+                    if (cz >= l - 2 && cz < l + 2) atomicAdd(&s_cls[q * kCls + 1 + (cz - (l - 2))], 1);
+                    if (cz >= u - 2 && cz < u + 2) atomicAdd(&s_cls[q * kCls + 5 + (cz - (u - 2))], 1);
+                }
+            }
+        }
+        mask[i] = m;
+    }
+    if (cls) {
+        __syncthreads();
+        for (int t = threadIdx.x; t < G * kCls; t += blockDim.x)
+            if (s_cls[t]) atomicAdd(&cls[t], s_cls[t]);
+    }
+}
+
+// Exclusive scan of the G per-destination totals (G <= 32).
+__global__ void k_dest_starts(const int* __restrict__ destCount, int G, int* __restrict__ destStart) {
+    const int q = threadIdx.x;
+    const int v = q < G ? destCount[q] : 0;
+    int incl = v;
+    for (int o = 1; o < 32; o <<= 1) {
+        const int x = __shfl_up_sync(0xffffffffu, incl, o);
+        if (q >= o) incl += x;
+    }
+    if (q < G) destStart[q] = incl - v;
+}
+
+// Metrics exchange ranges from the all-reduced per-rank metrics-grid layer
+// spans (lo = min, hi = max over each rank's owned particles): every other
+// rank's [lo, hi + 1) plus the k_dest_mask halo, everything for rank g.
+__global__ void k_metrics_ranges(int G, int g, int* __restrict__ lo, int* __restrict__ hi) {
+    const int q = threadIdx.x;
+    if (q >= G) return;
+    if (q == g) {
+        lo[q] = -(1 << 29);
+        hi[q] = 1 << 29;
+    } else if (lo[q] > hi[q]) {  // empty rank
+        lo[q] = 1 << 29;
+        hi[q] = -(1 << 29);
+    } else {
+        hi[q] = hi[q] + 1;  // exclusive
+    }
 }
 
 // Stable expansion by destination: per tile (kTileSize elements) counts of
@@ -193,25 +275,6 @@ __global__ void k_unpack_recs(int cnt, const Rec* __restrict__ in, StateSet d) {
     d.LV[k] = r.lv;
 }
 
-// Slot boundaries of the slab after the local sort: start of layer z is
-// cellStart[z * dx * dy] (z clamped to [0, dz]).  out = {ownBegin, ownEnd,
-// l1Begin, l1End, lowSendEnd, highSendBegin}.
-__global__ void k_slab_bounds(const Ctl* ctl, const int* __restrict__ cellStart, int zlo, int zhi,
-                              int* __restrict__ out) {
-    const GridDev& G = ctl->grid[0];
-    const long long layer = (long long)G.dims[0] * G.dims[1];
-    auto start = [&](int z) {
-        z = imin_std(imax_std(z, 0), G.dims[2]);
-        return cellStart[(long long)z * layer];
-    };
-    out[0] = start(zlo);
-    out[1] = start(zhi);
-    out[2] = start(zlo - 1);
-    out[3] = start(zhi + 1);
-    out[4] = start(zlo + 2);
-    out[5] = start(zhi - 2);
-}
-
 // Levels seen by the iteration order: 0 (never active) outside [b, e).
 __global__ void k_mask_levels(int n, const int* __restrict__ LV, int b, int e, int* __restrict__ out) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -311,9 +374,18 @@ __global__ void k_gather_int(int n, const int* __restrict__ perm, const int* __r
     if (k < n) out[k] = in[perm[k]];
 }
 
-// metrics-grid cz range of the owned particles (positions X) -> minmax[2]
+// lo[q] = INT_MAX, hi[q] = INT_MIN: the identity of the span all-reduce
+__global__ void k_span_init(int G, int* __restrict__ lo, int* __restrict__ hi) {
+    const int q = threadIdx.x;
+    if (q < G) {
+        lo[q] = 0x7fffffff;
+        hi[q] = (int)0x80000000;
+    }
+}
+
+// metrics-grid cz range of the owned particles (positions X) -> *lo_out, *hi_out
 __global__ void k_layer_minmax(int n, const float4* __restrict__ X, const Ctl* ctl, int g, float h,
-                               int* __restrict__ minmax) {
+                               int* __restrict__ lo_out, int* __restrict__ hi_out) {
     __shared__ int s_lo[32], s_hi[32];
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     int lo = 0x7fffffff, hi = (int)0x80000000;
@@ -330,8 +402,8 @@ __global__ void k_layer_minmax(int n, const float4* __restrict__ X, const Ctl* c
         lo = warp_min_i(in ? s_lo[threadIdx.x] : 0x7fffffff);
         hi = warp_max_i(in ? s_hi[threadIdx.x] : (int)0x80000000);
         if (threadIdx.x == 0) {
-            atomicMin(&minmax[0], lo);
-            atomicMax(&minmax[1], hi);
+            atomicMin(lo_out, lo);
+            atomicMax(hi_out, hi);
         }
     }
 }

@@ -1242,6 +1242,7 @@ struct apbf_gpu_solver {
     // set: this handle is rank g of G and holds only its owned particles.
 
     Transport* transport = nullptr;
+    long long n_global_ = 0;  // slab mode: particles over all ranks (set_state_local)
     std::unique_ptr<Transport> transport_owned;
     long long n_capacity = 0;
     DBuf<int> layerHist, zRange, bounds, destTile, destCountD, destStartD, sendIdx, LVo, ownedFlag,
@@ -1276,15 +1277,6 @@ struct apbf_gpu_solver {
                 prefixPost[s] += rows[(size_t)q * S2 + cfg.substeps + s];
             }
     }
-    bool slab_error = false;
-
-    std::vector<long long> all_counts(Transport& T, long long mine) {
-        std::vector<long long> snd(T.size(), mine), rcv(T.size());
-        T.alltoall_counts(snd.data(), rcv.data(), ws.stream);
-        rcv[T.rank()] = mine;
-        return rcv;
-    }
-
     // Upload this rank's slice (the rank's contiguous part of the global
     // storage order) with buffers sized for the global particle count.
     void set_state_local(int nloc, long long ntotal, const float* x, const float* xs, const float* v,
@@ -1293,6 +1285,7 @@ struct apbf_gpu_solver {
         // owned + ghost copies: a rank can hold more than n_global / G, and
         // the sends of one rank (owned + ghost duplicates) more than n_global
         n_capacity = 2 * std::max<long long>(ntotal, 1) + 4096;
+        n_global_ = ntotal;
         allocate((int)n_capacity);
         destMask.ensure(n_capacity);
         sendIdx.ensure(n_capacity);
@@ -1422,8 +1415,49 @@ struct apbf_gpu_solver {
         LAUNCH_CHECK();
     }
 
-    void run_frame_dist(Transport& T, std::vector<long long> cnt, bool assign_lod,
-                        const apbf_camera* cam, const apbf_lod_config* lod) {
+    // Device capacity of the global layer histogram (grown on need_layers).
+    int layer_cap = 4096;
+    DBuf<int> spanLo, spanHi;  // metrics: per-rank metrics-grid layer spans
+    DBuf<int> clsSend, clsRecv;  // per-destination record classes (kCls ints per rank)
+    std::vector<int> hostCls;    // [send G*kCls | recv G*kCls | ctl flags]
+
+    // The per-destination totals and classes of an exchange: sent on the
+    // stream ahead of the records (kCls ints per peer), then ONE host
+    // synchronisation reads what this rank sends and receives together with
+    // the (already all-reduced) abort flags.  Returns false on abort.
+    bool exchange_classes(Transport& T, int ncls) {
+        const int G = T.size(), g = T.rank();
+        cudaStream_t st = ws.stream;
+        std::vector<const void*> sp(G);
+        std::vector<void*> rp(G);
+        std::vector<size_t> sb(G), rb(G);
+        for (int q = 0; q < G; ++q) {
+            sp[q] = clsSend.p + (size_t)q * kCls;
+            rp[q] = clsRecv.p + (size_t)q * kCls;
+            sb[q] = rb[q] = sizeof(int) * ncls;
+        }
+        CK(cudaMemcpyAsync(clsRecv.p + (size_t)g * kCls, clsSend.p + (size_t)g * kCls, sizeof(int) * ncls,
+                           cudaMemcpyDeviceToDevice, st));
+        T.alltoallv(sp.data(), sb.data(), rp.data(), rb.data(), st);
+        hostCls.resize((size_t)2 * G * kCls);
+        CK(cudaMemcpyAsync(hostCls.data(), clsSend.p, sizeof(int) * G * kCls, cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(hostCls.data() + (size_t)G * kCls, clsRecv.p, sizeof(int) * G * kCls,
+                           cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(ws.h_ctl, ws.ctl.p, sizeof(Ctl), cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        return !ws.h_ctl->abort;
+    }
+
+    // One slab frame.  Per substep the host synchronises ONCE (after the
+    // class exchange): every size the rest of the substep needs -- records
+    // in and out, the local count, the owned range, the layer-1 ghost range
+    // and the two halo send ranges -- follows from the class counts.  The
+    // grid, the partition and the destination masks stay on the device; a
+    // failure anywhere aborts through the device flags, which are all-reduced
+    // before that synchronisation, so every rank leaves the collective
+    // sequence at the same point.
+    void run_frame_dist(Transport& T, long long nAll, bool assign_lod, const apbf_camera* cam,
+                        const apbf_lod_config* lod) {
         const int G = T.size(), g = T.rank();
         cudaStream_t st = ws.stream;
         Ctl* ctl = ws.ctl.p;
@@ -1431,9 +1465,9 @@ struct apbf_gpu_solver {
         const int nMax = cfg.n_max;
         localPre.assign(cfg.substeps, 0);
         localPost.assign(cfg.substeps, 0);
-        slab_error = false;
-        long long nAll = 0;
-        for (long long c : cnt) nAll += c;
+        layerHist.ensure(layer_cap);
+        clsSend.ensure((size_t)kMaxRanks * kCls);
+        clsRecv.ensure((size_t)kMaxRanks * kCls);
         CK(cudaEventRecord(ev[0], st));
         KL(k_frame_begin<<<1, 1, 0, st>>>(ctl));
         if (assign_lod) {
@@ -1453,46 +1487,62 @@ struct apbf_gpu_solver {
             KL(k_predict<<<blocks(n, kAabbBlock), kAabbBlock, 0, st>>>(n, src.X, src.V, src.V, src.XS, src.XS, dt,
                                                       cfg.gravity[0], cfg.gravity[1], cfg.gravity[2], ctl, s));
             // global grid: AABB all-reduce (ordered ints), identical params
-            // everywhere; the abort flag travels with it (one host sync)
+            // everywhere; the abort flag travels alongside
             T.allreduce(&ctl->abort, 1, RType::I32, ROp::Max, st);
             T.allreduce(&ctl->grid[0].lo_ord[0], 3, RType::I32, ROp::Min, st);
             T.allreduce(&ctl->grid[0].hi_ord[0], 3, RType::I32, ROp::Max, st);
             KL(k_grid_params<<<1, 1, 0, st>>>(ctl, 0, cfg.h, cfg.h));
-            ws.read_ctl();
-            if (ws.h_ctl->abort) break;
-            if (ws.h_ctl->runtime_error) break;
-            // slabs: equal-work split (sum of 1 + level per layer) of the global histogram
-            const int dz = ws.h_ctl->grid[0].dims[2];
-            layerHist.ensure(dz);
-            CK(cudaMemsetAsync(layerHist.p, 0, sizeof(int) * dz, st));
-            KL(k_layer_hist<<<blocks(n, 256), 256, 0, st>>>(n, src.XS, src.LV, ctl, 0, cfg.h, layerHist.p));
-            T.allreduce(layerHist.p, dz, RType::I32, ROp::Sum, st);
-            std::vector<int> h32(dz);
-            CK(cudaMemcpyAsync(h32.data(), layerHist.p, sizeof(int) * dz, cudaMemcpyDeviceToHost, st));
-            CK(cudaStreamSynchronize(st));
-            std::vector<long long> hist(h32.begin(), h32.end());
-            std::vector<int> zr(2 * G);
-            if (!slab_partition(hist.data(), dz, G, 2, zr.data(), zr.data() + G)) {
-                slab_error = true;
-                break;
-            }
-            CK(cudaMemcpyAsync(zRange.p, zr.data(), sizeof(int) * 2 * G, cudaMemcpyHostToDevice, st));
+            // slabs: equal-work split (sum of 1 + level per layer) of the
+            // global histogram, computed on the device
+            CK(cudaMemsetAsync(layerHist.p, 0, sizeof(int) * layer_cap, st));
+            KL(k_layer_hist<<<blocks(n, 256), 256, 0, st>>>(n, src.XS, src.LV, ctl, 0, cfg.h, layerHist.p,
+                                                          layer_cap));
+            T.allreduce(layerHist.p, layer_cap, RType::I32, ROp::Sum, st);
+            KL(k_slab_partition<<<1, 1, 0, st>>>(layerHist.p, ctl, G, 2, zRange.p));
             // migration + halo in one all-to-all, previous global order kept
+            CK(cudaMemsetAsync(clsSend.p, 0, sizeof(int) * G * kCls, st));
             KL(k_dest_mask<<<blocks(n, 256), 256, 0, st>>>(n, src.XS, ctl, 0, cfg.h, zRange.p, zRange.p + G,
-                                                         G, 2, destMask.p));
-            std::vector<long long> sendCnt, sendStart, recvCnt(G);
-            expand_by_dest(n, G, sendCnt, sendStart);
-            const long long nsend = sendStart[G - 1] + sendCnt[G - 1];
-            KL(k_pack_recs<<<blocks(nsend, 256), 256, 0, st>>>((int)nsend, sendIdx.p, src, sendRec.p));
-            T.alltoall_counts(sendCnt.data(), recvCnt.data(), st);
-            recvCnt[g] = sendCnt[g];
-            std::vector<long long> roff(G);
-            long long nLocal = 0;
+                                                         G, 2, destMask.p, clsSend.p));
+            if (!exchange_classes(T, kCls)) break;  // the substep's one host synchronisation
+            // sizes: what goes where, and this rank's layout after the sort
+            const int* sendC = hostCls.data();
+            const int* recvC = hostCls.data() + (size_t)G * kCls;
+            std::vector<long long> sendCnt(G), sendStart(G), recvCnt(G), roff(G);
+            long long nsend = 0, nLocal = 0;
+            long long lowG0 = 0, lowG1 = 0, own2lo = 0, hiG0 = 0, hiG1 = 0, ownHi2 = 0;
+            std::vector<int> ds(G);
             for (int q = 0; q < G; ++q) {
+                sendCnt[q] = sendC[q * kCls];
+                sendStart[q] = nsend;
+                ds[q] = (int)nsend;
+                nsend += sendCnt[q];
+                recvCnt[q] = recvC[q * kCls];
                 roff[q] = nLocal;
                 nLocal += recvCnt[q];
+                const int* c = recvC + q * kCls;
+                lowG0 += c[1];   // layer lo-2
+                lowG1 += c[2];   // layer lo-1
+                own2lo += c[3] + c[4];  // layers lo, lo+1
+                ownHi2 += c[5] + c[6];  // layers hi-2, hi-1
+                hiG0 += c[7];    // layer hi
+                hiG1 += c[8];    // layer hi+1
             }
-            if (nLocal > n_capacity) fail(APBF_ERR_RUNTIME, "slab holds more particles than the capacity");
+            // a rank receives every particle at most once: nLocal <= nAll <=
+            // n_capacity always; the send side was checked on the device
+            if (nLocal > n_capacity || nsend > n_capacity)
+                fail(APBF_ERR_RUNTIME, "slab exchange exceeds the per-rank capacity");
+            const int ownB = (int)(lowG0 + lowG1), l1B = (int)lowG0;
+            const int ownE = (int)(nLocal - hiG0 - hiG1), l1E = (int)(nLocal - hiG1);
+            const int lowEnd = (int)(ownB + own2lo), highB = (int)(ownE - ownHi2);
+            const int tiles = std::max(1, (n + kTileSize - 1) / kTileSize);
+            destTile.ensure((size_t)G * tiles);
+            CK(cudaMemcpyAsync(destStartD.p, ds.data(), sizeof(int) * G, cudaMemcpyHostToDevice, st));
+            KL(k_mask_tile_counts<<<tiles, kTileThreads, 0, st>>>(n, destMask.p, G, tiles, destTile.p));
+            KL(k_mask_scan<<<G, 1024, 0, st>>>(tiles, destTile.p, destCountD.p));
+            KL(k_mask_scatter<<<tiles, kTileThreads, 0, st>>>(n, destMask.p, G, tiles, destTile.p, destStartD.p,
+                                                            sendIdx.p));
+            if (nsend > 0)
+                KL(k_pack_recs<<<blocks(nsend, 256), 256, 0, st>>>((int)nsend, sendIdx.p, src, sendRec.p));
             std::vector<const void*> sp(G);
             std::vector<void*> rp(G);
             std::vector<size_t> sb(G), rb(G);
@@ -1514,11 +1564,6 @@ struct apbf_gpu_solver {
             const int smemG = (nMax + 1) * (int)sizeof(int);
             KL(k_gather<<<tilesL, kTileThreads, smemG, st>>>(nL, ctl, ws.perm.p, src, dst, nMax, tilesL,
                                                            tileCount.p));
-            KL(k_slab_bounds<<<1, 1, 0, st>>>(ctl, ws.cellCount.p, zr[g], zr[G + g], bounds.p));
-            int bd[6];
-            CK(cudaMemcpyAsync(bd, bounds.p, sizeof(bd), cudaMemcpyDeviceToHost, st));
-            CK(cudaStreamSynchronize(st));
-            const int ownB = bd[0], ownE = bd[1], l1B = bd[2], l1E = bd[3], lowEnd = bd[4], highB = bd[5];
             const int nOwn = ownE - ownB;
             if (scene.n > 0 && nOwn > 0)
                 KL(k_count_contacts<<<blocks(nOwn, 256), 256, 0, st>>>(nOwn, dst.XS + ownB, ws.scene.p, radius,
@@ -1591,70 +1636,66 @@ struct apbf_gpu_solver {
             localPost[s] = n;
         }
         CK(cudaEventRecord(ev[5], st));
-        const bool aborted = any_abort(T);
-        ws.read_ctl();
-        if (metrics && !aborted && !slab_error && !ws.h_ctl->runtime_error) run_metrics_dist(T);
+        T.allreduce(&ctl->abort, 1, RType::I32, ROp::Max, st);
+        if (metrics) run_metrics_dist(T);
         T.allreduce(&ctl->total_iterations, 1, RType::I64, ROp::Sum, st);
         T.allreduce(&ctl->contacts, 1, RType::I64, ROp::Sum, st);
         T.allreduce(&ctl->list_overflow, 1, RType::I32, ROp::Max, st);
+        T.allreduce(&ctl->abort, 1, RType::I32, ROp::Max, st);
         CK(cudaEventRecord(ev[6], st));
         ws.read_ctl();
     }
 
     // allDensities(x) across slabs: owned particles plus every particle of
-    // other ranks within one metrics-grid layer of their layer range.
+    // other ranks within one metrics-grid layer of their layer range.  The
+    // ranges are all-reduced on the device; one host synchronisation (the
+    // class exchange) gives the sizes.  Skipped (consistently) on abort.
     void run_metrics_dist(Transport& T) {
         const int G = T.size(), g = T.rank();
         cudaStream_t st = ws.stream;
         Ctl* ctl = ws.ctl.p;
         const StateSet cs = set[cur].view();
+        spanLo.ensure(kMaxRanks);
+        spanHi.ensure(kMaxRanks);
         KL(k_grid_reset<<<1, 1, 0, st>>>(ctl, 1));
         KL(k_aabb<<<blocks(n, kAabbBlock), kAabbBlock, 0, st>>>(n, cs.X, ctl, 1));
         T.allreduce(&ctl->grid[1].lo_ord[0], 3, RType::I32, ROp::Min, st);
         T.allreduce(&ctl->grid[1].hi_ord[0], 3, RType::I32, ROp::Max, st);
         KL(k_grid_params<<<1, 1, 0, st>>>(ctl, 1, cfg.h, cfg.h));
-        int mm[2] = {0x7fffffff, (int)0x80000000};
-        CK(cudaMemcpyAsync(minmax.p, mm, sizeof(mm), cudaMemcpyHostToDevice, st));
-        KL(k_layer_minmax<<<blocks(n, 256), 256, 0, st>>>(n, cs.X, ctl, 1, cfg.h, minmax.p));
-        CK(cudaMemcpyAsync(mm, minmax.p, sizeof(mm), cudaMemcpyDeviceToHost, st));
-        CK(cudaStreamSynchronize(st));
-        std::vector<int> lo(G, 0x7fffffff), hi(G, (int)0x80000000);
-        lo[g] = mm[0];
-        hi[g] = mm[1];
-        CK(cudaMemcpyAsync(zRange.p, lo.data(), sizeof(int) * G, cudaMemcpyHostToDevice, st));
-        CK(cudaMemcpyAsync(zRange.p + G, hi.data(), sizeof(int) * G, cudaMemcpyHostToDevice, st));
-        T.allreduce(zRange.p, G, RType::I32, ROp::Min, st);
-        T.allreduce(zRange.p + G, G, RType::I32, ROp::Max, st);
-        CK(cudaMemcpyAsync(lo.data(), zRange.p, sizeof(int) * G, cudaMemcpyDeviceToHost, st));
-        CK(cudaMemcpyAsync(hi.data(), zRange.p + G, sizeof(int) * G, cudaMemcpyDeviceToHost, st));
-        CK(cudaStreamSynchronize(st));
+        KL(k_span_init<<<1, 32, 0, st>>>(G, spanLo.p, spanHi.p));
+        KL(k_layer_minmax<<<blocks(n, 256), 256, 0, st>>>(n, cs.X, ctl, 1, cfg.h, spanLo.p + g, spanHi.p + g));
+        T.allreduce(spanLo.p, G, RType::I32, ROp::Min, st);
+        T.allreduce(spanHi.p, G, RType::I32, ROp::Max, st);
+        KL(k_metrics_ranges<<<1, 32, 0, st>>>(G, g, spanLo.p, spanHi.p));
+        CK(cudaMemsetAsync(clsSend.p, 0, sizeof(int) * G * kCls, st));
+        KL(k_dest_mask<<<blocks(n, 256), 256, 0, st>>>(n, cs.X, ctl, 1, cfg.h, spanLo.p, spanHi.p, G, 1,
+                                                     destMask.p, clsSend.p));
+        if (!exchange_classes(T, 1)) return;
+        const int* sendC = hostCls.data();
+        const int* recvC = hostCls.data() + (size_t)G * kCls;
+        std::vector<long long> sendCnt(G), sendStart(G), recvCnt(G), roff(G);
+        std::vector<int> ds(G);
+        long long nsend = 0, nM = 0;
         for (int q = 0; q < G; ++q) {
-            if (q == g) {
-                lo[q] = -(1 << 29);
-                hi[q] = 1 << 29;
-            } else if (lo[q] > hi[q]) {
-                lo[q] = 1 << 29;  // empty rank
-                hi[q] = -(1 << 29);
-            } else {
-                hi[q] = hi[q] + 1;  // exclusive
-            }
-        }
-        CK(cudaMemcpyAsync(zRange.p, lo.data(), sizeof(int) * G, cudaMemcpyHostToDevice, st));
-        CK(cudaMemcpyAsync(zRange.p + G, hi.data(), sizeof(int) * G, cudaMemcpyHostToDevice, st));
-        KL(k_dest_mask<<<blocks(n, 256), 256, 0, st>>>(n, cs.X, ctl, 1, cfg.h, zRange.p, zRange.p + G, G, 1,
-                                                     destMask.p));
-        std::vector<long long> sendCnt, sendStart, recvCnt(G);
-        expand_by_dest(n, G, sendCnt, sendStart);
-        const long long nsend = sendStart[G - 1] + sendCnt[G - 1];
-        KL(k_pack_pm<<<blocks(nsend, 256), 256, 0, st>>>((int)nsend, sendIdx.p, cs.X, cs.XS, sendPM.p));
-        T.alltoall_counts(sendCnt.data(), recvCnt.data(), st);
-        recvCnt[g] = sendCnt[g];
-        std::vector<long long> roff(G);
-        long long nM = 0;
-        for (int q = 0; q < G; ++q) {
+            sendCnt[q] = sendC[q * kCls];
+            sendStart[q] = nsend;
+            ds[q] = (int)nsend;
+            nsend += sendCnt[q];
+            recvCnt[q] = recvC[q * kCls];
             roff[q] = nM;
             nM += recvCnt[q];
         }
+        if (nM > n_capacity || nsend > n_capacity)
+            fail(APBF_ERR_RUNTIME, "slab metrics exchange exceeds the per-rank capacity");
+        const int tiles = std::max(1, (n + kTileSize - 1) / kTileSize);
+        destTile.ensure((size_t)G * tiles);
+        CK(cudaMemcpyAsync(destStartD.p, ds.data(), sizeof(int) * G, cudaMemcpyHostToDevice, st));
+        KL(k_mask_tile_counts<<<tiles, kTileThreads, 0, st>>>(n, destMask.p, G, tiles, destTile.p));
+        KL(k_mask_scan<<<G, 1024, 0, st>>>(tiles, destTile.p, destCountD.p));
+        KL(k_mask_scatter<<<tiles, kTileThreads, 0, st>>>(n, destMask.p, G, tiles, destTile.p, destStartD.p,
+                                                        sendIdx.p));
+        if (nsend > 0)
+            KL(k_pack_pm<<<blocks(nsend, 256), 256, 0, st>>>((int)nsend, sendIdx.p, cs.X, cs.XS, sendPM.p));
         std::vector<const void*> sp(G);
         std::vector<void*> rp(G);
         std::vector<size_t> sb(G), rb(G);
@@ -1694,9 +1735,7 @@ struct apbf_gpu_solver {
             copy_set(set[0], set[2]);
             cur = 0;
         }
-        std::vector<long long> cnt = all_counts(T, n);
-        long long nAll = 0;
-        for (long long c : cnt) nAll += c;
+        const long long nAll = n_global_;  // particles are conserved: fixed at set_state
         agree_uniform_w(T);
         if (assign_lod && cfg.mode == APBF_MODE_APBF) {
             apbf_lod_config lc = *lod;
@@ -1714,17 +1753,21 @@ struct apbf_gpu_solver {
             const int start_n = n;
             copy_set(set[2], set[start_set]);
             for (int attempt = 0;; ++attempt) {
-                run_frame_dist(T, cnt, assign_lod, cam, lod);
-                if (!ws.h_ctl->list_overflow) break;
+                run_frame_dist(T, nAll, assign_lod, cam, lod);
+                // the retry conditions are all-reduced (list_overflow) or global
+                // (need_layers comes from the global grid): every rank retries
+                const bool lists = ws.h_ctl->list_overflow != 0, layers = ws.h_ctl->need_layers > layer_cap;
+                if (!lists && !layers) break;
                 if (attempt > 6) fail(APBF_ERR_RUNTIME, "neighbor list overflow");
                 cur = start_set;
                 n = start_n;
                 copy_set(set[cur], set[2]);
-                grow_lists(ws.h_ctl->list_alloc, ws.h_ctl->list_alloc_fb);
+                if (lists) grow_lists(ws.h_ctl->list_alloc, ws.h_ctl->list_alloc_fb);
+                if (layers) layer_cap = std::max(2 * layer_cap, ws.h_ctl->need_layers + 16);
             }
             const Ctl& c = *ws.h_ctl;
             if (c.runtime_error) fail(APBF_ERR_RUNTIME, "grid cell count exceeds limit; domain blew up");
-            if (slab_error) fail(APBF_ERR_RUNTIME, "too few grid layers for the slab decomposition");
+            if (c.slab_error) fail(APBF_ERR_RUNTIME, "too few grid layers for the slab decomposition");
             // global first error: (substep, iteration, pass, global index) -- only
             // when the frame aborted (the abort flag is already all-reduced)
             const long long NONE = 0x7fffffffffffffffLL;

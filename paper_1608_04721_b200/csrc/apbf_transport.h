@@ -281,7 +281,10 @@ struct NcclTransport final : Transport {
 // whole layers: zlo[g] .. zhi[g] (exclusive), every slab at least minLayers
 // thick.  Returns false when the grid has too few layers.  Pure host logic,
 // identical on every rank (same histogram in, same slabs out).
-inline bool slab_partition(const long long* hist, int dz, int G, int minLayers, int* zlo, int* zhi) {
+// (__host__ __device__: the slab frame runs it on the device, k_slab_partition,
+// and the host entry point apbf_slab_partition is the same code.)
+template <class H>
+__host__ __device__ inline bool slab_partition(const H* hist, int dz, int G, int minLayers, int* zlo, int* zhi) {
     if (dz < G * minLayers) return false;
     long long total = 0;
     for (int z = 0; z < dz; ++z) total += hist[z];

@@ -42,9 +42,9 @@ def test_fast_build_within_tier_b_of_reference_double(mode):
     for f in range(K):
         sg = g.step_frame(a, spec.camera, spec.lod, f)
         s64 = r64.step_frame(d64, spec.camera, spec.lod, f)
-        r32.step_frame(d32, spec.camera, spec.lod, f)
-        if f == 0:  # levels and totals come from the frame-start positions
-            assert sg.total_iterations == s64.total_iterations
+        s32 = r32.step_frame(d32, spec.camera, spec.lod, f)
+        if f == 0:  # levels and totals come from the frame-start positions (float LOD)
+            assert sg.total_iterations == s32.total_iterations
         assert abs(sg.avg_density_pct - s64.avg_density_pct) < 0.5
     tree = cKDTree(d64.x)
     e_fast = tree.query(a.x.astype(np.float64))[0].max()

@@ -139,7 +139,7 @@ def swirl_state(n_side=12, h=0.1, seed=1):
 
 # eq. 15 carries no particle volume, so |omega| ~ curl / V (~1e4 here) and a
 # physically sized eps is ~1e-4 (dv = dt eps |omega| ~ 1 cm/s per substep)
-@pytest.mark.parametrize("xsph,eps", [(0.01, 0.0), (0.0, 2e-4), (0.05, 1e-3)])
+@pytest.mark.parametrize("xsph,eps", [(2e-5, 0.0), (0.0, 2e-4), (1e-5, 1e-3)])
 def test_post_pass_matches_paper_equations(xsph, eps):
     x0, v0, mass = swirl_state()
     base = SolverConfig(h=0.1, substeps=1, range=IterationRange(3, 3), gravity=(0.0, -9.81, 0.0))
@@ -210,17 +210,23 @@ def test_confinement_keeps_a_vortex_spinning():
 
 
 def test_xsph_smooths_relative_velocity():
-    """XSPH (eq. 17) pulls each velocity toward its neighbours' mean: the
-    velocity noise about the swirl shrinks."""
+    """XSPH (eq. 17) pulls each velocity toward its neighbours': the velocity
+    noise about the swirl shrinks.  Eq. 17 carries no particle volume either
+    (sum_j W ~ 1.5e4 here), so a stable c is ~1e-5; the density solve is
+    relaxed away as above.  (Oracle + paper_post_pass on the host: mean
+    deviation 0.088 -> 0.062 after 3 frames at c = 2e-5.)"""
     x0, v0, mass = swirl_state(12, 0.1, seed=3)
-    base = SolverConfig(h=0.1, substeps=1, range=IterationRange(2, 2), gravity=(0.0, 0.0, 0.0))
-    on = SolverConfig(**{**base.__dict__, "xsph_viscosity": 0.1})
+    base = SolverConfig(h=0.1, substeps=1, dt_frame=0.0008, range=IterationRange(2, 2), gravity=(0.0, 0.0, 0.0),
+                        epsilon=1e12)
+    on = SolverConfig(**{**base.__dict__, "xsph_viscosity": 2e-5})
     out = []
     for cfg in (base, on):
         st = ParticleSet(x0, 1.0, 2)
         st.v, st.mass, st.inv_mass = v0.copy(), mass.copy(), (F(1) / mass).astype(F)
-        Solver(cfg).step_frame_with_levels(st, 0)
+        sv = Solver(cfg)
+        for f in range(3):
+            sv.step_frame_with_levels(st, f)
         nb = brute_neighbors(st.x, cfg.h)
         dev = [np.linalg.norm(st.v[i] - st.v[nb[i]].mean(0)) for i in range(len(nb)) if len(nb[i])]
         out.append(float(np.mean(dev)))
-    assert out[1] < 0.9 * out[0]
+    assert out[1] < 0.8 * out[0], out
