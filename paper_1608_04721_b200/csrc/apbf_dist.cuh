@@ -275,35 +275,54 @@ __global__ void k_unpack_recs(int cnt, const Rec* __restrict__ in, StateSet d) {
     d.LV[k] = r.lv;
 }
 
-// Levels seen by the iteration order: 0 (never active) outside [b, e).
-__global__ void k_mask_levels(int n, const int* __restrict__ LV, int b, int e, int* __restrict__ out) {
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < n) out[i] = (i >= b && i < e) ? LV[i] : 0;
-}
-
-// Per-tile level histogram (the part of k_gather the slab path needs on the
-// masked levels).
-__global__ void __launch_bounds__(kTileThreads) k_level_tiles(int n, const Ctl* ctl, const int* __restrict__ LV,
-                                                              int nMax, int numTiles,
-                                                              int* __restrict__ tileCount) {
-    if (ctl->abort) return;
-    extern __shared__ int s_cnt[];
-    for (int l = threadIdx.x; l <= nMax; l += blockDim.x) s_cnt[l] = 0;
-    __syncthreads();
-    for (int r = 0; r < kTileRounds; ++r) {
-        const int k = blockIdx.x * kTileSize + r * kTileThreads + threadIdx.x;
-        if (k < n) atomicAdd(&s_cnt[imin_std(imax_std(LV[k], 0), nMax)], 1);
+// One all-reduce instead of three for the substep's grid: [~abort, lo(3),
+// ~hi(3)] all-reduced with MIN (bitwise not reverses the order of ordered
+// ints without overflow), then written back.
+__global__ void k_grid_reduce_pack(const Ctl* ctl, int g, int* __restrict__ buf) {
+    const GridDev& G = ctl->grid[g];
+    buf[0] = ~ctl->abort;
+    for (int a = 0; a < 3; ++a) {
+        buf[1 + a] = G.lo_ord[a];
+        buf[4 + a] = ~G.hi_ord[a];
     }
-    __syncthreads();
-    for (int l = threadIdx.x; l <= nMax; l += blockDim.x)
-        tileCount[(long long)l * numTiles + blockIdx.x] = s_cnt[l];
+}
+__global__ void k_grid_reduce_unpack(Ctl* ctl, int g, const int* __restrict__ buf) {
+    GridDev& G = ctl->grid[g];
+    ctl->abort = ~buf[0];
+    for (int a = 0; a < 3; ++a) {
+        G.lo_ord[a] = buf[1 + a];
+        G.hi_ord[a] = ~buf[4 + a];
+    }
 }
 
-// sum of levels over [b, e) (the owned particles' particle-iterations).
-__global__ void k_level_sum(int b, int e, const int* __restrict__ LV, Ctl* ctl) {
+// The owned slice [b, b + m) of the sorted set back to the front of the
+// other set (this rank's state for the next substep): all six fields in one
+// launch.
+__global__ void k_copy_owned(int m, int b, StateSet from, StateSet to) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= m) return;
+    to.X[i] = from.X[b + i];
+    to.V[i] = from.V[b + i];
+    to.XS[i] = from.XS[b + i];
+    to.W[i] = from.W[b + i];
+    to.L[i] = from.L[b + i];
+    to.LV[i] = from.LV[b + i];
+}
+
+// Contacts (findContacts().size(), sdf.hpp:226-250) and the level sum
+// (particle-iterations, solver.hpp:311-313) of the owned slots [b, e) in
+// one pass.
+__global__ void k_owned_counts(int b, int e, const float4* __restrict__ XS, const int* __restrict__ LV,
+                               const Scene* __restrict__ scene, float r, int contacts, Ctl* ctl) {
     __shared__ int s_part[32];
     const int i = b + blockIdx.x * blockDim.x + threadIdx.x;
-    int v = warp_sum_i(i < e ? LV[i] : 0);
+    const bool in = i < e;
+    bool c = false;
+    if (in && contacts) {
+        const float4 p = XS[i];
+        c = scene_phi(*scene, p.x, p.y, p.z) < r;
+    }
+    int v = warp_sum_i(in ? LV[i] : 0);
     if ((threadIdx.x & 31) == 0) s_part[threadIdx.x >> 5] = v;
     __syncthreads();
     if (threadIdx.x < 32) {  // one atomic per block
@@ -311,6 +330,30 @@ __global__ void k_level_sum(int b, int e, const int* __restrict__ LV, Ctl* ctl) 
         v = warp_sum_i(v);
         if (threadIdx.x == 0 && v) atomicAdd(&ctl->total_iterations, (unsigned long long)v);
     }
+    if (contacts) block_count_add(&ctl->contacts, c);
+}
+
+// The iteration order's levels (0, never active, outside the owned +
+// layer-1 ghost range [b, e)) and their per-tile histogram, in one pass.
+__global__ void __launch_bounds__(kTileThreads) k_mask_level_tiles(int n, const Ctl* ctl,
+                                                                   const int* __restrict__ LV, int b, int e,
+                                                                   int* __restrict__ LVo, int nMax, int numTiles,
+                                                                   int* __restrict__ tileCount) {
+    if (ctl->abort) return;
+    extern __shared__ int s_cnt[];
+    for (int l = threadIdx.x; l <= nMax; l += blockDim.x) s_cnt[l] = 0;
+    __syncthreads();
+    for (int r = 0; r < kTileRounds; ++r) {
+        const int k = blockIdx.x * kTileSize + r * kTileThreads + threadIdx.x;
+        if (k < n) {
+            const int lv = (k >= b && k < e) ? LV[k] : 0;
+            LVo[k] = lv;
+            atomicAdd(&s_cnt[imin_std(imax_std(lv, 0), nMax)], 1);
+        }
+    }
+    __syncthreads();
+    for (int l = threadIdx.x; l <= nMax; l += blockDim.x)
+        tileCount[(long long)l * numTiles + blockIdx.x] = s_cnt[l];
 }
 
 // Metrics ghost records: (x, y, z, mass) + owned flag in the w of a second

@@ -463,6 +463,8 @@ struct apbf_gpu_solver {
         activeCount.ensure(cfg.n_max + 2);
         bucketStart.ensure(cfg.n_max + 2);
         resid.ensure((size_t)cfg.substeps * cfg.n_max);
+        chunkCtr.ensure((size_t)cfg.substeps * cfg.n_max * 2);
+        if (const char* v = std::getenv("APBF_DYN")) dyn_mode = std::atoi(v);
     }
     ~apbf_gpu_solver() {
         drop_graph();
@@ -602,31 +604,59 @@ struct apbf_gpu_solver {
     // (fast_pair_coef), outside the bitwise contract
     bool fast_math = false;
 
+    // Dynamic chunk claiming in the solver passes (for_chunks): a resident-
+    // size grid claims CTA-sized chunks of the active range from a per-launch
+    // counter (chunkCtr, zeroed once per frame), so an iteration with a small
+    // active set launches no empty CTAs.  dyn_mode: 0 static grids, 1 dynamic
+    // for the iterations past n_min (partly active), 2 dynamic everywhere.
+    int dyn_mode = 1;
+    DBuf<int> chunkCtr;
+    int resident_l = 0, resident_d = 0;  // resident CTAs of the lambda / delta-p kernels
+    int* chunk_slot(int s, int it, int pass) {
+        if (dyn_mode == 0 || (dyn_mode == 1 && it <= cfg.n_min)) return nullptr;
+        return chunkCtr.p + ((size_t)s * cfg.n_max + (it - 1)) * 2 + pass;
+    }
+    template <class KFn>
+    static int resident_ctas(KFn kern, int threads) {
+        int per_sm = 0;
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, 0));
+        int dev = 0, sms = 0;
+        CK(cudaGetDevice(&dev));
+        CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+        return std::max(1, per_sm) * sms;
+    }
+
     template <bool kZ, bool kF>
     void launch_pair_t(int it, int s, const float4* Pc, float4* Pn, const StateSet& dst,
                        const SolverConsts& sc, int tslot) {
         cudaStream_t st = ws.stream;
         Ctl* ctl = ws.ctl.p;
-        const int sb = blocks(n_iter, kLambdaThreads);
-        constexpr int B = kLambdaThreads, K = kBatch;
+        constexpr int B = kLambdaThreads, K = kBatch, D = kDeltapThreads;
+        int* dl = chunk_slot(s, it, 0);
+        int* dd = chunk_slot(s, it, 1);
+        if (dl && !resident_l) {
+            resident_l = resident_ctas(k_lambda<B, K, kZ, 2, kF>, B);
+            resident_d = resident_ctas(k_deltap_apply<kZ, D, K, kF>, D);
+        }
+        const int sb = dl ? std::min(blocks(n_iter, B), resident_l) : blocks(n_iter, B);
+        const int sd = dd ? std::min(blocks(n_iter, D), resident_d) : blocks(n_iter, D);
         // inverse-mass specialisations (w_mode, checked at upload)
         if (w_mode == 2)
             KL(k_lambda<B, K, kZ, 2, kF><<<sb, B, 0, st>>>(n_iter, it, ctl, activeCount.p, order.p, Pc, dst.W,
                                                           dst.L, nbr.p, nbrCount.p, groupBase.p, sc, s, ownB_,
-                                                          ownE_, PL.p));
+                                                          ownE_, PL.p, dl));
         else if (w_mode == 1)
             KL(k_lambda<B, K, kZ, 1, kF><<<sb, B, 0, st>>>(n_iter, it, ctl, activeCount.p, order.p, Pc, dst.W,
                                                           dst.L, nbr.p, nbrCount.p, groupBase.p, sc, s, ownB_,
-                                                          ownE_, PL.p));
+                                                          ownE_, PL.p, dl));
         else
             KL(k_lambda<B, K, kZ, 0, kF><<<sb, B, 0, st>>>(n_iter, it, ctl, activeCount.p, order.p, Pc, dst.W,
                                                           dst.L, nbr.p, nbrCount.p, groupBase.p, sc, s, ownB_,
-                                                          ownE_, PL.p));
+                                                          ownE_, PL.p, dl));
         if (tslot >= 0) rec(kt_ev[tslot][1]);
-        constexpr int D = kDeltapThreads;
-        KL(k_deltap_apply<kZ, D, K, kF><<<blocks(n_iter, D), D, 0, st>>>(
+        KL(k_deltap_apply<kZ, D, K, kF><<<sd, D, 0, st>>>(
             n_iter, it, ctl, activeCount.p, order.p, Pc, Pn, dst.W, dst.L, dst.LV, nbr.p, nbrCount.p,
-            groupBase.p, ws.scene.p, sc, s, ownB_, ownE_, PL.p));
+            groupBase.p, ws.scene.p, sc, s, ownB_, ownE_, PL.p, dd));
     }
 
     // The list build and the residual pass.
@@ -669,7 +699,7 @@ struct apbf_gpu_solver {
         const int lvl = (kMaxLevels + 1) * (int)sizeof(int);
         CK(cudaFuncSetAttribute(k_level_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, 9 * lvl));
         CK(cudaFuncSetAttribute(k_gather, cudaFuncAttributeMaxDynamicSharedMemorySize, lvl));
-        CK(cudaFuncSetAttribute(k_level_tiles, cudaFuncAttributeMaxDynamicSharedMemorySize, lvl));
+        CK(cudaFuncSetAttribute(k_mask_level_tiles, cudaFuncAttributeMaxDynamicSharedMemorySize, lvl));
         cudaGetLastError();
     }
 
@@ -732,6 +762,7 @@ struct apbf_gpu_solver {
         kt_used = 0;
         n_iter = n;
         KL(k_frame_begin<<<1, 1, 0, st>>>(ctl));
+        CK(cudaMemsetAsync(chunkCtr.p, 0, sizeof(int) * chunkCtr.n, st));
         if (assign_lod) {
             if (cfg.mode == APBF_MODE_PBF) {
                 KL(k_fill_int<<<blocks(n, 256), 256, 0, st>>>(set[cur].LV.p, n, nMax));
@@ -1023,7 +1054,7 @@ struct apbf_gpu_solver {
         k.ktime = kernel_timing;
         k.ptime = phase_timing;
         k.n = n;
-        k.flags = (w_mode << 20) | (packed_lists ? 0x400000 : 0) | (fast_math ? 1 : 0);
+        k.flags = (w_mode << 20) | (packed_lists ? 0x400000 : 0) | (fast_math ? 1 : 0) | (dyn_mode << 1);
         k.caps[0] = nbrCap;
         k.stride = list_stride;
         if (w_mode == 2) std::memcpy(&k.w0bits, &w0, sizeof w0);
@@ -1343,34 +1374,6 @@ struct apbf_gpu_solver {
         if (sync) CK(cudaStreamSynchronize(st));  // the caller may reuse its arrays on return
     }
 
-    // Stable expansion of the `n` current particles by destination mask:
-    // returns per-destination counts and fills sendIdx (grouped by dest).
-    void expand_by_dest(int nn, int G, std::vector<long long>& cnt, std::vector<long long>& start) {
-        cudaStream_t st = ws.stream;
-        const int tiles = std::max(1, (nn + kTileSize - 1) / kTileSize);
-        destTile.ensure((size_t)G * tiles);
-        KL(k_mask_tile_counts<<<tiles, kTileThreads, 0, st>>>(nn, destMask.p, G, tiles, destTile.p));
-        KL(k_mask_scan<<<G, 1024, 0, st>>>(tiles, destTile.p, destCountD.p));
-        std::vector<int> c(G);
-        CK(cudaMemcpyAsync(c.data(), destCountD.p, sizeof(int) * G, cudaMemcpyDeviceToHost, st));
-        CK(cudaStreamSynchronize(st));
-        cnt.assign(G, 0);
-        start.assign(G, 0);
-        long long acc = 0;
-        std::vector<int> ds(G);
-        for (int q = 0; q < G; ++q) {
-            cnt[q] = c[q];
-            start[q] = acc;
-            ds[q] = (int)acc;
-            acc += c[q];
-        }
-        if (acc > n_capacity) fail(APBF_ERR_RUNTIME, "slab exchange exceeds the per-rank capacity");
-        CK(cudaMemcpyAsync(destStartD.p, ds.data(), sizeof(int) * G, cudaMemcpyHostToDevice, st));
-        KL(k_mask_scatter<<<tiles, kTileThreads, 0, st>>>(nn, destMask.p, G, tiles, destTile.p, destStartD.p,
-                                                        sendIdx.p));
-        LAUNCH_CHECK();
-    }
-
     bool any_abort(Transport& T) {
         T.allreduce(&ws.ctl.p->abort, 1, RType::I32, ROp::Max, ws.stream);
         int a = 0;
@@ -1415,10 +1418,42 @@ struct apbf_gpu_solver {
         LAUNCH_CHECK();
     }
 
+    // APBF_SLAB_TRACE=1: host enqueue time vs device time of the slab frame's
+    // phases on stderr (where the decomposition's overhead goes).
+    struct TracePt {
+        const char* what;
+        std::chrono::steady_clock::time_point host;
+        cudaEvent_t ev;
+    };
+    std::vector<TracePt> trace_;
+    bool slab_trace = std::getenv("APBF_SLAB_TRACE") != nullptr;
+    void tmark(const char* what) {
+        if (!slab_trace) return;
+        TracePt t{what, std::chrono::steady_clock::now(), nullptr};
+        CK(cudaEventCreate(&t.ev));
+        CK(cudaEventRecord(t.ev, ws.stream));
+        trace_.push_back(t);
+    }
+    void tflush() {
+        if (!slab_trace || trace_.empty()) return;
+        CK(cudaEventSynchronize(trace_.back().ev));
+        for (size_t k = 1; k < trace_.size(); ++k) {
+            float d = 0.f;
+            cudaEventElapsedTime(&d, trace_[k - 1].ev, trace_[k].ev);
+            const double hms = std::chrono::duration<double, std::milli>(trace_[k].host - trace_[k - 1].host).count();
+            std::fprintf(stderr, "[slab] %-22s host %.3f ms  device %.3f ms\n", trace_[k].what, hms, d);
+        }
+        for (auto& t : trace_) cudaEventDestroy(t.ev);
+        trace_.clear();
+    }
+
     // Device capacity of the global layer histogram (grown on need_layers).
     int layer_cap = 4096;
     DBuf<int> spanLo, spanHi;  // metrics: per-rank metrics-grid layer spans
-    DBuf<int> clsSend, clsRecv;  // per-destination record classes (kCls ints per rank)
+    DBuf<int> clsBuf;            // per-destination record classes: [sent G*kCls | received G*kCls]
+    int* clsSend = nullptr;
+    int* clsRecv = nullptr;
+    DBuf<int> gridRed;           // [~abort, lo(3), ~hi(3)]: the grid's one MIN all-reduce
     std::vector<int> hostCls;    // [send G*kCls | recv G*kCls | ctl flags]
 
     // The per-destination totals and classes of an exchange: sent on the
@@ -1432,17 +1467,15 @@ struct apbf_gpu_solver {
         std::vector<void*> rp(G);
         std::vector<size_t> sb(G), rb(G);
         for (int q = 0; q < G; ++q) {
-            sp[q] = clsSend.p + (size_t)q * kCls;
-            rp[q] = clsRecv.p + (size_t)q * kCls;
+            sp[q] = clsSend + (size_t)q * kCls;
+            rp[q] = clsRecv + (size_t)q * kCls;
             sb[q] = rb[q] = sizeof(int) * ncls;
         }
-        CK(cudaMemcpyAsync(clsRecv.p + (size_t)g * kCls, clsSend.p + (size_t)g * kCls, sizeof(int) * ncls,
+        CK(cudaMemcpyAsync(clsRecv + (size_t)g * kCls, clsSend + (size_t)g * kCls, sizeof(int) * ncls,
                            cudaMemcpyDeviceToDevice, st));
         T.alltoallv(sp.data(), sb.data(), rp.data(), rb.data(), st);
         hostCls.resize((size_t)2 * G * kCls);
-        CK(cudaMemcpyAsync(hostCls.data(), clsSend.p, sizeof(int) * G * kCls, cudaMemcpyDeviceToHost, st));
-        CK(cudaMemcpyAsync(hostCls.data() + (size_t)G * kCls, clsRecv.p, sizeof(int) * G * kCls,
-                           cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(hostCls.data(), clsSend, sizeof(int) * 2 * G * kCls, cudaMemcpyDeviceToHost, st));
         CK(cudaMemcpyAsync(ws.h_ctl, ws.ctl.p, sizeof(Ctl), cudaMemcpyDeviceToHost, st));
         CK(cudaStreamSynchronize(st));
         return !ws.h_ctl->abort;
@@ -1466,10 +1499,14 @@ struct apbf_gpu_solver {
         localPre.assign(cfg.substeps, 0);
         localPost.assign(cfg.substeps, 0);
         layerHist.ensure(layer_cap);
-        clsSend.ensure((size_t)kMaxRanks * kCls);
-        clsRecv.ensure((size_t)kMaxRanks * kCls);
+        gridRed.ensure(8);
+        clsBuf.ensure((size_t)2 * kMaxRanks * kCls);
+        clsSend = clsBuf.p;
+        clsRecv = clsBuf.p + (size_t)G * kCls;
         CK(cudaEventRecord(ev[0], st));
+        tmark("start");
         KL(k_frame_begin<<<1, 1, 0, st>>>(ctl));
+        CK(cudaMemsetAsync(chunkCtr.p, 0, sizeof(int) * chunkCtr.n, st));
         if (assign_lod) {
             if (cfg.mode == APBF_MODE_PBF) {
                 KL(k_fill_int<<<blocks(n, 256), 256, 0, st>>>(set[cur].LV.p, n, nMax));
@@ -1480,6 +1517,7 @@ struct apbf_gpu_solver {
                 run_lod_dist(T, set[cur].X.p, n, nAll, *cam, lc, set[cur].LV.p);
             }
         }
+        tmark("lod");
         for (int s = 0; s < cfg.substeps; ++s) {
             localPre[s] = n;
             StateSet src = set[cur].view(), dst = set[cur ^ 1].view();
@@ -1488,9 +1526,9 @@ struct apbf_gpu_solver {
                                                       cfg.gravity[0], cfg.gravity[1], cfg.gravity[2], ctl, s));
             // global grid: AABB all-reduce (ordered ints), identical params
             // everywhere; the abort flag travels alongside
-            T.allreduce(&ctl->abort, 1, RType::I32, ROp::Max, st);
-            T.allreduce(&ctl->grid[0].lo_ord[0], 3, RType::I32, ROp::Min, st);
-            T.allreduce(&ctl->grid[0].hi_ord[0], 3, RType::I32, ROp::Max, st);
+            KL(k_grid_reduce_pack<<<1, 1, 0, st>>>(ctl, 0, gridRed.p));
+            T.allreduce(gridRed.p, 7, RType::I32, ROp::Min, st);
+            KL(k_grid_reduce_unpack<<<1, 1, 0, st>>>(ctl, 0, gridRed.p));
             KL(k_grid_params<<<1, 1, 0, st>>>(ctl, 0, cfg.h, cfg.h));
             // slabs: equal-work split (sum of 1 + level per layer) of the
             // global histogram, computed on the device
@@ -1500,21 +1538,21 @@ struct apbf_gpu_solver {
             T.allreduce(layerHist.p, layer_cap, RType::I32, ROp::Sum, st);
             KL(k_slab_partition<<<1, 1, 0, st>>>(layerHist.p, ctl, G, 2, zRange.p));
             // migration + halo in one all-to-all, previous global order kept
-            CK(cudaMemsetAsync(clsSend.p, 0, sizeof(int) * G * kCls, st));
+            CK(cudaMemsetAsync(clsSend, 0, sizeof(int) * G * kCls, st));
             KL(k_dest_mask<<<blocks(n, 256), 256, 0, st>>>(n, src.XS, ctl, 0, cfg.h, zRange.p, zRange.p + G,
-                                                         G, 2, destMask.p, clsSend.p));
+                                                         G, 2, destMask.p, clsSend));
+            tmark("pre-exchange");
             if (!exchange_classes(T, kCls)) break;  // the substep's one host synchronisation
+            tmark("class sync");
             // sizes: what goes where, and this rank's layout after the sort
             const int* sendC = hostCls.data();
             const int* recvC = hostCls.data() + (size_t)G * kCls;
             std::vector<long long> sendCnt(G), sendStart(G), recvCnt(G), roff(G);
             long long nsend = 0, nLocal = 0;
             long long lowG0 = 0, lowG1 = 0, own2lo = 0, hiG0 = 0, hiG1 = 0, ownHi2 = 0;
-            std::vector<int> ds(G);
             for (int q = 0; q < G; ++q) {
                 sendCnt[q] = sendC[q * kCls];
                 sendStart[q] = nsend;
-                ds[q] = (int)nsend;
                 nsend += sendCnt[q];
                 recvCnt[q] = recvC[q * kCls];
                 roff[q] = nLocal;
@@ -1536,9 +1574,9 @@ struct apbf_gpu_solver {
             const int lowEnd = (int)(ownB + own2lo), highB = (int)(ownE - ownHi2);
             const int tiles = std::max(1, (n + kTileSize - 1) / kTileSize);
             destTile.ensure((size_t)G * tiles);
-            CK(cudaMemcpyAsync(destStartD.p, ds.data(), sizeof(int) * G, cudaMemcpyHostToDevice, st));
             KL(k_mask_tile_counts<<<tiles, kTileThreads, 0, st>>>(n, destMask.p, G, tiles, destTile.p));
             KL(k_mask_scan<<<G, 1024, 0, st>>>(tiles, destTile.p, destCountD.p));
+            KL(k_dest_starts<<<1, 32, 0, st>>>(destCountD.p, G, destStartD.p));
             KL(k_mask_scatter<<<tiles, kTileThreads, 0, st>>>(n, destMask.p, G, tiles, destTile.p, destStartD.p,
                                                             sendIdx.p));
             if (nsend > 0)
@@ -1558,6 +1596,7 @@ struct apbf_gpu_solver {
             T.alltoallv(sp.data(), sb.data(), rp.data(), rb.data(), st);
             const int nL = (int)nLocal;
             KL(k_unpack_recs<<<blocks(nL, 256), 256, 0, st>>>(nL, recvRec.p, src));
+            tmark("exchange");
             // local stable sort by global cell == global order restricted
             ws.run_grid(0, src.XS, nL, cfg.h, cfg.h, false, radius);
             const int tilesL = std::max(1, (nL + kTileSize - 1) / kTileSize);
@@ -1565,14 +1604,13 @@ struct apbf_gpu_solver {
             KL(k_gather<<<tilesL, kTileThreads, smemG, st>>>(nL, ctl, ws.perm.p, src, dst, nMax, tilesL,
                                                            tileCount.p));
             const int nOwn = ownE - ownB;
-            if (scene.n > 0 && nOwn > 0)
-                KL(k_count_contacts<<<blocks(nOwn, 256), 256, 0, st>>>(nOwn, dst.XS + ownB, ws.scene.p, radius,
-                                                                     ctl));
-            if (nOwn > 0) KL(k_level_sum<<<blocks(nOwn, 256), 256, 0, st>>>(ownB, ownE, dst.LV, ctl));
+            if (nOwn > 0)
+                KL(k_owned_counts<<<blocks(nOwn, 256), 256, 0, st>>>(ownB, ownE, dst.XS, dst.LV, ws.scene.p, radius,
+                                                                   scene.n > 0 ? 1 : 0, ctl));
             // iteration order over owned + layer-1 ghosts (lambda is computed
             // redundantly for the latter), outer ghosts never active
-            KL(k_mask_levels<<<blocks(nL, 256), 256, 0, st>>>(nL, dst.LV, l1B, l1E, LVo.p));
-            KL(k_level_tiles<<<tilesL, kTileThreads, smemG, st>>>(nL, ctl, LVo.p, nMax, tilesL, tileCount.p));
+            KL(k_mask_level_tiles<<<tilesL, kTileThreads, smemG, st>>>(nL, ctl, dst.LV, l1B, l1E, LVo.p, nMax,
+                                                                      tilesL, tileCount.p));
             KL(k_level_scan<<<nMax + 1, 1024, 0, st>>>(ctl, tilesL, tileCount.p, levelCount.p));
             KL(k_level_finish<<<1, 32, 0, st>>>(ctl, nL, nMax, levelCount.p, activeCount.p, bucketStart.p, 0));
             KL(k_level_scatter<<<tilesL, kTileThreads, 9 * smemG, st>>>(nL, ctl, LVo.p, nMax, tilesL,
@@ -1585,6 +1623,7 @@ struct apbf_gpu_solver {
                                                                        ws.scene.p, radius, cfg.stab_iterations,
                                                                        s, ownB, ownE));
             LAUNCH_CHECK();
+            tmark("sort+lists");
             ownB_ = ownB;
             ownE_ = ownE;
             n_iter = nL;
@@ -1615,6 +1654,7 @@ struct apbf_gpu_solver {
                 }
                 T.alltoallv(hs.data(), hsb.data(), hr.data(), hrb.data(), st);
             }
+            tmark("iterations");
             ownB_ = 0;
             ownE_ = 0x7fffffff;
             float4* Pf = P[nMax & 1];
@@ -1623,17 +1663,10 @@ struct apbf_gpu_solver {
                                                                dst.V + ownB, dt, cap, Pf != dst.XS ? 1 : 0, s));
             LAUNCH_CHECK();
             // keep only the owned particles, in order, as this rank's state
-            const size_t m = (size_t)nOwn;
-            if (m > 0) {
-                CK(cudaMemcpyAsync(src.X, dst.X + ownB, sizeof(float4) * m, cudaMemcpyDeviceToDevice, st));
-                CK(cudaMemcpyAsync(src.V, dst.V + ownB, sizeof(float4) * m, cudaMemcpyDeviceToDevice, st));
-                CK(cudaMemcpyAsync(src.XS, dst.XS + ownB, sizeof(float4) * m, cudaMemcpyDeviceToDevice, st));
-                CK(cudaMemcpyAsync(src.W, dst.W + ownB, sizeof(float) * m, cudaMemcpyDeviceToDevice, st));
-                CK(cudaMemcpyAsync(src.L, dst.L + ownB, sizeof(float) * m, cudaMemcpyDeviceToDevice, st));
-                CK(cudaMemcpyAsync(src.LV, dst.LV + ownB, sizeof(int) * m, cudaMemcpyDeviceToDevice, st));
-            }
+            if (nOwn > 0) KL(k_copy_owned<<<blocks(nOwn, 256), 256, 0, st>>>(nOwn, ownB, dst, src));
             n = nOwn;
             localPost[s] = n;
+            tmark("finalize+copy");
         }
         CK(cudaEventRecord(ev[5], st));
         T.allreduce(&ctl->abort, 1, RType::I32, ROp::Max, st);
@@ -1643,7 +1676,9 @@ struct apbf_gpu_solver {
         T.allreduce(&ctl->list_overflow, 1, RType::I32, ROp::Max, st);
         T.allreduce(&ctl->abort, 1, RType::I32, ROp::Max, st);
         CK(cudaEventRecord(ev[6], st));
+        tmark("metrics+reduce");
         ws.read_ctl();
+        tflush();
     }
 
     // allDensities(x) across slabs: owned particles plus every particle of
@@ -1659,27 +1694,26 @@ struct apbf_gpu_solver {
         spanHi.ensure(kMaxRanks);
         KL(k_grid_reset<<<1, 1, 0, st>>>(ctl, 1));
         KL(k_aabb<<<blocks(n, kAabbBlock), kAabbBlock, 0, st>>>(n, cs.X, ctl, 1));
-        T.allreduce(&ctl->grid[1].lo_ord[0], 3, RType::I32, ROp::Min, st);
-        T.allreduce(&ctl->grid[1].hi_ord[0], 3, RType::I32, ROp::Max, st);
+        KL(k_grid_reduce_pack<<<1, 1, 0, st>>>(ctl, 1, gridRed.p));
+        T.allreduce(gridRed.p, 7, RType::I32, ROp::Min, st);
+        KL(k_grid_reduce_unpack<<<1, 1, 0, st>>>(ctl, 1, gridRed.p));
         KL(k_grid_params<<<1, 1, 0, st>>>(ctl, 1, cfg.h, cfg.h));
         KL(k_span_init<<<1, 32, 0, st>>>(G, spanLo.p, spanHi.p));
         KL(k_layer_minmax<<<blocks(n, 256), 256, 0, st>>>(n, cs.X, ctl, 1, cfg.h, spanLo.p + g, spanHi.p + g));
         T.allreduce(spanLo.p, G, RType::I32, ROp::Min, st);
         T.allreduce(spanHi.p, G, RType::I32, ROp::Max, st);
         KL(k_metrics_ranges<<<1, 32, 0, st>>>(G, g, spanLo.p, spanHi.p));
-        CK(cudaMemsetAsync(clsSend.p, 0, sizeof(int) * G * kCls, st));
+        CK(cudaMemsetAsync(clsSend, 0, sizeof(int) * G * kCls, st));
         KL(k_dest_mask<<<blocks(n, 256), 256, 0, st>>>(n, cs.X, ctl, 1, cfg.h, spanLo.p, spanHi.p, G, 1,
-                                                     destMask.p, clsSend.p));
+                                                     destMask.p, clsSend));
         if (!exchange_classes(T, 1)) return;
         const int* sendC = hostCls.data();
         const int* recvC = hostCls.data() + (size_t)G * kCls;
         std::vector<long long> sendCnt(G), sendStart(G), recvCnt(G), roff(G);
-        std::vector<int> ds(G);
         long long nsend = 0, nM = 0;
         for (int q = 0; q < G; ++q) {
             sendCnt[q] = sendC[q * kCls];
             sendStart[q] = nsend;
-            ds[q] = (int)nsend;
             nsend += sendCnt[q];
             recvCnt[q] = recvC[q * kCls];
             roff[q] = nM;
@@ -1689,9 +1723,9 @@ struct apbf_gpu_solver {
             fail(APBF_ERR_RUNTIME, "slab metrics exchange exceeds the per-rank capacity");
         const int tiles = std::max(1, (n + kTileSize - 1) / kTileSize);
         destTile.ensure((size_t)G * tiles);
-        CK(cudaMemcpyAsync(destStartD.p, ds.data(), sizeof(int) * G, cudaMemcpyHostToDevice, st));
         KL(k_mask_tile_counts<<<tiles, kTileThreads, 0, st>>>(n, destMask.p, G, tiles, destTile.p));
         KL(k_mask_scan<<<G, 1024, 0, st>>>(tiles, destTile.p, destCountD.p));
+        KL(k_dest_starts<<<1, 32, 0, st>>>(destCountD.p, G, destStartD.p));
         KL(k_mask_scatter<<<tiles, kTileThreads, 0, st>>>(n, destMask.p, G, tiles, destTile.p, destStartD.p,
                                                         sendIdx.p));
         if (nsend > 0)

@@ -2,7 +2,7 @@
 (--metrics gpu__time_duration.sum CSV) and key counters from --set full reports.
 
 usage: python tools/ncu_summary.py --launches gpurun_out/launches.csv \
-          --full gpurun_out/prof_lambda.ncu-rep [...] --out profiles/r01
+          --full [label=]gpurun_out/prof_lambda.ncu-rep [...] --out profiles/r02
 """
 import argparse, collections, csv, json, os, subprocess, sys
 
@@ -44,7 +44,7 @@ def launches(path, frames_from_end=2):
                         for k, v in sorted(tot.items(), key=lambda x: -x[1])}}
 
 
-def full(path):
+def full(path, label=None):
     out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(out.splitlines()))
     h, units = rows[0], rows[1]
@@ -58,7 +58,7 @@ def full(path):
         rd = float(r[h.index("dram__bytes_read.sum")]) * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}[units[h.index("dram__bytes_read.sum")]]
         wr = float(r[h.index("dram__bytes_write.sum")]) * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}[units[h.index("dram__bytes_write.sum")]]
         d["dram_bytes_per_launch"] = rd + wr
-        res[name.split("<")[0]] = d
+        res[label or name.split("<")[0]] = d
     return res
 
 
@@ -72,8 +72,9 @@ if __name__ == "__main__":
     if a.launches:
         summary["launch_list"] = launches(a.launches)
     summary["kernels"] = {}
-    for f in a.full:
-        summary["kernels"].update(full(f))
+    for f in a.full:  # path, or label=path (e.g. k_lambda_fast=gpurun_out/prof_k_lambda_fast.ncu-rep)
+        label, _, path = f.rpartition("=")
+        summary["kernels"].update(full(path, label or None))
     os.makedirs(os.path.dirname(a.out) or ".", exist_ok=True)
     json.dump(summary, open(a.out + ".json", "w"), indent=1)
     print(json.dumps(summary, indent=1)[:3000])
