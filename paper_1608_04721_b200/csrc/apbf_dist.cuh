@@ -333,11 +333,12 @@ __global__ void k_owned_counts(int b, int e, const float4* __restrict__ XS, cons
     if (contacts) block_count_add(&ctl->contacts, c);
 }
 
-// The iteration order's levels (0, never active, outside the owned +
-// layer-1 ghost range [b, e)) and their per-tile histogram, in one pass.
+// The iteration order's levels (0, never active, outside [b, e) or inside
+// the excluded [xb, xe)) and their per-tile histogram, in one pass.
 __global__ void __launch_bounds__(kTileThreads) k_mask_level_tiles(int n, const Ctl* ctl,
                                                                    const int* __restrict__ LV, int b, int e,
-                                                                   int* __restrict__ LVo, int nMax, int numTiles,
+                                                                   int xb, int xe, int* __restrict__ LVo,
+                                                                   int nMax, int numTiles,
                                                                    int* __restrict__ tileCount) {
     if (ctl->abort) return;
     extern __shared__ int s_cnt[];
@@ -346,7 +347,7 @@ __global__ void __launch_bounds__(kTileThreads) k_mask_level_tiles(int n, const 
     for (int r = 0; r < kTileRounds; ++r) {
         const int k = blockIdx.x * kTileSize + r * kTileThreads + threadIdx.x;
         if (k < n) {
-            const int lv = (k >= b && k < e) ? LV[k] : 0;
+            const int lv = (k >= b && k < e && !(k >= xb && k < xe)) ? LV[k] : 0;
             LVo[k] = lv;
             atomicAdd(&s_cnt[imin_std(imax_std(lv, 0), nMax)], 1);
         }

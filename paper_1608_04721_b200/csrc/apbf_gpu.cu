@@ -463,8 +463,7 @@ struct apbf_gpu_solver {
         activeCount.ensure(cfg.n_max + 2);
         bucketStart.ensure(cfg.n_max + 2);
         resid.ensure((size_t)cfg.substeps * cfg.n_max);
-        chunkCtr.ensure((size_t)cfg.substeps * cfg.n_max * 2);
-        if (const char* v = std::getenv("APBF_DYN")) dyn_mode = std::atoi(v);
+
     }
     ~apbf_gpu_solver() {
         drop_graph();
@@ -473,6 +472,9 @@ struct apbf_gpu_solver {
         if (ev_vm) cudaEventDestroy(ev_vm);
         if (ev_inputs) cudaEventDestroy(ev_inputs);
         if (copy_stream) cudaStreamDestroy(copy_stream);
+        if (comm_stream) cudaStreamDestroy(comm_stream);
+        if (ev_halo_ready) cudaEventDestroy(ev_halo_ready);
+        if (ev_halo_done) cudaEventDestroy(ev_halo_done);
     }
 
     void allocate(int nn) {
@@ -604,59 +606,33 @@ struct apbf_gpu_solver {
     // (fast_pair_coef), outside the bitwise contract
     bool fast_math = false;
 
-    // Dynamic chunk claiming in the solver passes (for_chunks): a resident-
-    // size grid claims CTA-sized chunks of the active range from a per-launch
-    // counter (chunkCtr, zeroed once per frame), so an iteration with a small
-    // active set launches no empty CTAs.  dyn_mode: 0 static grids, 1 dynamic
-    // for the iterations past n_min (partly active), 2 dynamic everywhere.
-    int dyn_mode = 1;
-    DBuf<int> chunkCtr;
-    int resident_l = 0, resident_d = 0;  // resident CTAs of the lambda / delta-p kernels
-    int* chunk_slot(int s, int it, int pass) {
-        if (dyn_mode == 0 || (dyn_mode == 1 && it <= cfg.n_min)) return nullptr;
-        return chunkCtr.p + ((size_t)s * cfg.n_max + (it - 1)) * 2 + pass;
-    }
-    template <class KFn>
-    static int resident_ctas(KFn kern, int threads) {
-        int per_sm = 0;
-        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, 0));
-        int dev = 0, sms = 0;
-        CK(cudaGetDevice(&dev));
-        CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-        return std::max(1, per_sm) * sms;
-    }
-
+    // which: 1 the lambda pass, 2 the delta-p pass, 3 both
     template <bool kZ, bool kF>
     void launch_pair_t(int it, int s, const float4* Pc, float4* Pn, const StateSet& dst,
-                       const SolverConsts& sc, int tslot) {
+                       const SolverConsts& sc, int tslot, int which) {
         cudaStream_t st = ws.stream;
         Ctl* ctl = ws.ctl.p;
         constexpr int B = kLambdaThreads, K = kBatch, D = kDeltapThreads;
-        int* dl = chunk_slot(s, it, 0);
-        int* dd = chunk_slot(s, it, 1);
-        if (dl && !resident_l) {
-            resident_l = resident_ctas(k_lambda<B, K, kZ, 2, kF>, B);
-            resident_d = resident_ctas(k_deltap_apply<kZ, D, K, kF>, D);
-        }
-        const int sb = dl ? std::min(blocks(n_iter, B), resident_l) : blocks(n_iter, B);
-        const int sd = dd ? std::min(blocks(n_iter, D), resident_d) : blocks(n_iter, D);
+        const int sb = blocks(n_iter, B), sd = blocks(n_iter, D);
         // inverse-mass specialisations (w_mode, checked at upload)
-        if (w_mode == 2)
+        if (!(which & 1)) {
+        } else if (w_mode == 2)
             KL(k_lambda<B, K, kZ, 2, kF><<<sb, B, 0, st>>>(n_iter, it, ctl, activeCount.p, order.p, Pc, dst.W,
                                                           dst.L, nbr.p, nbrCount.p, groupBase.p, sc, s, ownB_,
-                                                          ownE_, PL.p, dl));
+                                                          ownE_, PL.p));
         else if (w_mode == 1)
             KL(k_lambda<B, K, kZ, 1, kF><<<sb, B, 0, st>>>(n_iter, it, ctl, activeCount.p, order.p, Pc, dst.W,
                                                           dst.L, nbr.p, nbrCount.p, groupBase.p, sc, s, ownB_,
-                                                          ownE_, PL.p, dl));
+                                                          ownE_, PL.p));
         else
             KL(k_lambda<B, K, kZ, 0, kF><<<sb, B, 0, st>>>(n_iter, it, ctl, activeCount.p, order.p, Pc, dst.W,
                                                           dst.L, nbr.p, nbrCount.p, groupBase.p, sc, s, ownB_,
-                                                          ownE_, PL.p, dl));
+                                                          ownE_, PL.p));
         if (tslot >= 0) rec(kt_ev[tslot][1]);
-        KL(k_deltap_apply<kZ, D, K, kF><<<sd, D, 0, st>>>(
-            n_iter, it, ctl, activeCount.p, order.p, Pc, Pn, dst.W, dst.L, dst.LV, nbr.p, nbrCount.p,
-            groupBase.p, ws.scene.p, sc, s, ownB_, ownE_, PL.p, dd));
+        if (which & 2)
+            KL(k_deltap_apply<kZ, D, K, kF><<<sd, D, 0, st>>>(
+                n_iter, it, ctl, activeCount.p, order.p, Pc, Pn, dst.W, dst.L, dst.LV, nbr.p, nbrCount.p,
+                groupBase.p, ws.scene.p, sc, s, ownB_, ownE_, PL.p));
     }
 
     // The list build and the residual pass.
@@ -665,11 +641,11 @@ struct apbf_gpu_solver {
         if (packed_lists)
             KL(k_build_lists<<<blocks(nn, kListThreads), kListThreads, 0, st>>>(
                 nn, ws.ctl.p, order.p, dst.XS, ws.cellCount.p, cfg.h, cfg.h * cfg.h, nbr.p, nbrCount.p,
-                groupBase.p, nbrCap));
+                groupBase.p, nbrCap, activeCount.p + 1));
         else
             KL(k_build_lists_direct<<<blocks(nn, kListThreads), kListThreads, 0, st>>>(
                 nn, ws.ctl.p, order.p, dst.XS, ws.cellCount.p, cfg.h, cfg.h * cfg.h, nbr.p, nbrCount.p,
-                groupBase.p, list_stride));
+                groupBase.p, list_stride, activeCount.p + 1));
     }
     void launch_residual(int nn, int it, const float4* Pn, const SolverConsts& sc, double* out, int oB,
                          int oE) {
@@ -703,21 +679,56 @@ struct apbf_gpu_solver {
         cudaGetLastError();
     }
 
+    // which: 1 the lambda pass, 2 the delta-p pass, 3 both
     void launch_solver_pair(int it, int s, const float4* Pc, float4* Pn, const StateSet& dst,
-                            const SolverConsts& sc, int tslot) {
+                            const SolverConsts& sc, int tslot, int which = 3) {
         const int v = (cfg.inactive_lambda_zero ? 1 : 0) | (fast_math ? 2 : 0);
         switch (v) {
-            case 0: launch_pair_t<false, false>(it, s, Pc, Pn, dst, sc, tslot); break;
-            case 1: launch_pair_t<true, false>(it, s, Pc, Pn, dst, sc, tslot); break;
-            case 2: launch_pair_t<false, true>(it, s, Pc, Pn, dst, sc, tslot); break;
-            default: launch_pair_t<true, true>(it, s, Pc, Pn, dst, sc, tslot); break;
+            case 0: launch_pair_t<false, false>(it, s, Pc, Pn, dst, sc, tslot, which); break;
+            case 1: launch_pair_t<true, false>(it, s, Pc, Pn, dst, sc, tslot, which); break;
+            case 2: launch_pair_t<false, true>(it, s, Pc, Pn, dst, sc, tslot, which); break;
+            default: launch_pair_t<true, true>(it, s, Pc, Pn, dst, sc, tslot, which); break;
         }
+    }
+
+    // Slab mode: a second iteration set (order, level bucketing and frozen
+    // lists) for the halo-dependent particles, so that the interior's passes
+    // overlap the x* halo exchange.  swap_sets() exchanges the two sets'
+    // buffers; every launch helper works on the current one.
+    DBuf<int> orderB, nbrCountB, nbrB, levelCountB, activeCountB, bucketStartB;
+    DBuf<long long> groupBaseB;
+    static void swap_buf(DBuf<int>& a, DBuf<int>& b) {
+        std::swap(a.p, b.p);
+        std::swap(a.n, b.n);
+    }
+    void swap_sets() {
+        swap_buf(order, orderB);
+        swap_buf(nbrCount, nbrCountB);
+        swap_buf(nbr, nbrB);
+        swap_buf(levelCount, levelCountB);
+        swap_buf(activeCount, activeCountB);
+        swap_buf(bucketStart, bucketStartB);
+        std::swap(groupBase.p, groupBaseB.p);
+        std::swap(groupBase.n, groupBaseB.n);
+    }
+    void ensure_set_b() {
+        orderB.ensure(order.n);
+        nbrCountB.ensure(nbrCount.n);
+        nbrB.ensure(nbr.n);
+        levelCountB.ensure(levelCount.n);
+        activeCountB.ensure(activeCount.n);
+        bucketStartB.ensure(bucketStart.n);
+        groupBaseB.ensure(groupBase.n);
     }
 
     // (Re)allocate the order-based list store at nbrCap entries.
     void alloc_lists() {
         nbr.release();
         nbr.ensure((size_t)nbrCap);
+        if (nbrB.p) {  // slab mode's second iteration set follows
+            nbrB.release();
+            nbrB.ensure((size_t)nbrCap);
+        }
     }
 
     // After an overflowed list build: grow the per-lane stride, or switch to
@@ -762,7 +773,6 @@ struct apbf_gpu_solver {
         kt_used = 0;
         n_iter = n;
         KL(k_frame_begin<<<1, 1, 0, st>>>(ctl));
-        CK(cudaMemsetAsync(chunkCtr.p, 0, sizeof(int) * chunkCtr.n, st));
         if (assign_lod) {
             if (cfg.mode == APBF_MODE_PBF) {
                 KL(k_fill_int<<<blocks(n, 256), 256, 0, st>>>(set[cur].LV.p, n, nMax));
@@ -1054,7 +1064,7 @@ struct apbf_gpu_solver {
         k.ktime = kernel_timing;
         k.ptime = phase_timing;
         k.n = n;
-        k.flags = (w_mode << 20) | (packed_lists ? 0x400000 : 0) | (fast_math ? 1 : 0) | (dyn_mode << 1);
+        k.flags = (w_mode << 20) | (packed_lists ? 0x400000 : 0) | (fast_math ? 1 : 0);
         k.caps[0] = nbrCap;
         k.stride = list_stride;
         if (w_mode == 2) std::memcpy(&k.w0bits, &w0, sizeof w0);
@@ -1418,6 +1428,9 @@ struct apbf_gpu_solver {
         LAUNCH_CHECK();
     }
 
+    cudaStream_t comm_stream = nullptr;  // slab mode: the x* halo exchange (overlapped)
+    cudaEvent_t ev_halo_ready = nullptr, ev_halo_done = nullptr;
+
     // APBF_SLAB_TRACE=1: host enqueue time vs device time of the slab frame's
     // phases on stderr (where the decomposition's overhead goes).
     struct TracePt {
@@ -1506,7 +1519,6 @@ struct apbf_gpu_solver {
         CK(cudaEventRecord(ev[0], st));
         tmark("start");
         KL(k_frame_begin<<<1, 1, 0, st>>>(ctl));
-        CK(cudaMemsetAsync(chunkCtr.p, 0, sizeof(int) * chunkCtr.n, st));
         if (assign_lod) {
             if (cfg.mode == APBF_MODE_PBF) {
                 KL(k_fill_int<<<blocks(n, 256), 256, 0, st>>>(set[cur].LV.p, n, nMax));
@@ -1608,14 +1620,35 @@ struct apbf_gpu_solver {
                 KL(k_owned_counts<<<blocks(nOwn, 256), 256, 0, st>>>(ownB, ownE, dst.XS, dst.LV, ws.scene.p, radius,
                                                                    scene.n > 0 ? 1 : 0, ctl));
             // iteration order over owned + layer-1 ghosts (lambda is computed
-            // redundantly for the latter), outer ghosts never active
-            KL(k_mask_level_tiles<<<tilesL, kTileThreads, smemG, st>>>(nL, ctl, dst.LV, l1B, l1E, LVo.p, nMax,
-                                                                      tilesL, tileCount.p));
-            KL(k_level_scan<<<nMax + 1, 1024, 0, st>>>(ctl, tilesL, tileCount.p, levelCount.p));
-            KL(k_level_finish<<<1, 32, 0, st>>>(ctl, nL, nMax, levelCount.p, activeCount.p, bucketStart.p, 0));
-            KL(k_level_scatter<<<tilesL, kTileThreads, 9 * smemG, st>>>(nL, ctl, LVo.p, nMax, tilesL,
-                                                                       tileCount.p, bucketStart.p, order.p));
-            launch_build_lists(nL, dst);
+            // redundantly for the latter), outer ghosts never active.  With
+            // neighbours the particles split into two iteration sets: A, the
+            // interior owned layers [lo+2, hi-2), whose lambda never reads a
+            // ghost; B, the layer-1 ghosts and the owned layers the halo sends
+            // (lo, lo+1, hi-2, hi-1).  Per iteration: lambda(A) needs no halo;
+            // lambda(B) waits for the previous halo; delta-p(B) produces the
+            // x* the next halo sends, which then runs on comm_stream while
+            // delta-p(A) and the next lambda(A) compute.  (Same per-particle
+            // lists and sums: bitwise the single-set results.)
+            const int a0 = g > 0 ? lowEnd : ownB, a1 = g < G - 1 ? highB : ownE;
+            const bool split = G > 1 && !cfg.record_residuals && a0 < a1;
+            auto bucket = [&](int b, int e, int xb, int xe) {
+                KL(k_mask_level_tiles<<<tilesL, kTileThreads, smemG, st>>>(nL, ctl, dst.LV, b, e, xb, xe, LVo.p,
+                                                                          nMax, tilesL, tileCount.p));
+                KL(k_level_scan<<<nMax + 1, 1024, 0, st>>>(ctl, tilesL, tileCount.p, levelCount.p));
+                KL(k_level_finish<<<1, 32, 0, st>>>(ctl, nL, nMax, levelCount.p, activeCount.p, bucketStart.p, 0));
+                KL(k_level_scatter<<<tilesL, kTileThreads, 9 * smemG, st>>>(nL, ctl, LVo.p, nMax, tilesL,
+                                                                           tileCount.p, bucketStart.p, order.p));
+                launch_build_lists(nL, dst);
+            };
+            if (split) {
+                ensure_set_b();
+                bucket(a0, a1, 0, 0);  // set A
+                swap_sets();
+                bucket(l1B, l1E, a0, a1);  // set B
+                swap_sets();
+            } else {
+                bucket(l1B, l1E, 0, 0);
+            }
             // pre-stabilization of every local copy with level < S (owners and
             // ghost copies compute the same values); errors from owned only
             if (S > 1)
@@ -1628,10 +1661,25 @@ struct apbf_gpu_solver {
             ownE_ = ownE;
             n_iter = nL;
             float4* P[2] = {dst.XS, PB.p};
+            if (split && !comm_stream) {
+                CK(cudaStreamCreateWithFlags(&comm_stream, cudaStreamNonBlocking));
+                CK(cudaEventCreateWithFlags(&ev_halo_ready, cudaEventDisableTiming));
+                CK(cudaEventCreateWithFlags(&ev_halo_done, cudaEventDisableTiming));
+            }
             for (int it = 1; it <= nMax; ++it) {
                 const float4* Pc = P[(it - 1) & 1];
                 float4* Pn = P[it & 1];
-                launch_solver_pair(it, s, Pc, Pn, dst, sc, -1);
+                if (split) {
+                    launch_solver_pair(it, s, Pc, Pn, dst, sc, -1, 1);  // lambda(A)
+                    if (it > 1) CK(cudaStreamWaitEvent(st, ev_halo_done, 0));
+                    swap_sets();
+                    launch_solver_pair(it, s, Pc, Pn, dst, sc, -1, 3);  // lambda(B), delta-p(B)
+                    swap_sets();
+                    CK(cudaEventRecord(ev_halo_ready, st));
+                    CK(cudaStreamWaitEvent(comm_stream, ev_halo_ready, 0));
+                } else {
+                    launch_solver_pair(it, s, Pc, Pn, dst, sc, -1);
+                }
                 if (cfg.record_residuals) {
                     CK(cudaMemsetAsync(resid.p + (size_t)s * nMax + (it - 1), 0, sizeof(double), st));
                     launch_residual(nL, it, Pn, sc, resid.p + (size_t)s * nMax + (it - 1), ownB, ownE);
@@ -1652,8 +1700,15 @@ struct apbf_gpu_solver {
                     hr[g + 1] = Pn + ownE;
                     hrb[g + 1] = sizeof(float4) * (size_t)(nL - ownE);
                 }
-                T.alltoallv(hs.data(), hsb.data(), hr.data(), hrb.data(), st);
+                if (split) {
+                    T.alltoallv(hs.data(), hsb.data(), hr.data(), hrb.data(), comm_stream);
+                    CK(cudaEventRecord(ev_halo_done, comm_stream));
+                    launch_solver_pair(it, s, Pc, Pn, dst, sc, -1, 2);  // delta-p(A), overlapping the halo
+                } else {
+                    T.alltoallv(hs.data(), hsb.data(), hr.data(), hrb.data(), st);
+                }
             }
+            if (split) CK(cudaStreamWaitEvent(st, ev_halo_done, 0));  // the last halo landed
             tmark("iterations");
             ownB_ = 0;
             ownE_ = 0x7fffffff;

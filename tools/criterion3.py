@@ -1,7 +1,9 @@
-"""A/B of the solver passes' work distribution (APBF_DYN = 0 static grids, 1
-dynamic chunks past n_min, 2 dynamic everywhere): device ms/frame (LOD +
-substeps, FrameStats.wallMs median, metrics off) on the 1M ocean for PBF 10
-and APBF {5..10} DTC / DTVS, and the reference's criterion-3 reduction."""
+"""Criterion 3 of the reference (acceptance_main.cpp:136-163) on the B200:
+median device ms/frame (LOD + substeps, FrameStats.wallMs, metrics off) on
+the 1M ocean for PBF 10 and APBF {5..10} DTC / DTVS over `frames` frames
+(the reference measures 80, the settled regime), and the reduction
+(t_pbf - t_apbf) / t_pbf.  Extra args are APBF_* environment settings to
+A/B, e.g. `python tools/dyn_ab.py 80 APBF_GRAPHS=0`."""
 import os
 import statistics
 import sys
@@ -11,8 +13,10 @@ from paper_1608_04721_b200 import LodModel, Solver, SolverMode  # noqa: E402
 from paper_1608_04721_b200 import scenario as S  # noqa: E402
 
 frames = int(sys.argv[1]) if len(sys.argv) > 1 else 12
-for dyn in sys.argv[2:] or ["0", "1", "2"]:
-    os.environ["APBF_DYN"] = dyn
+for setting in sys.argv[2:] or ["default"]:
+    if "=" in setting:
+        k, v = setting.split("=", 1)
+        os.environ[k] = v
     res = {}
     for mode in ("pbf", "dtc", "dtvs"):
         spec = S.build_scenario("ocean_1m")
@@ -26,5 +30,5 @@ for dyn in sys.argv[2:] or ["0", "1", "2"]:
         ms = [sv.step_frame_resident(spec.camera, spec.lod, f).wall_ms for f in range(frames)]
         res[mode] = statistics.median(ms[3:])
     red = {m: (res["pbf"] - res[m]) / res["pbf"] for m in ("dtc", "dtvs")}
-    print(f"APBF_DYN={dyn}: pbf10 {res['pbf']:.3f} dtc {res['dtc']:.3f} dtvs {res['dtvs']:.3f} ms; "
+    print(f"{setting} ({frames} frames): pbf10 {res['pbf']:.3f} dtc {res['dtc']:.3f} dtvs {res['dtvs']:.3f} ms; "
           f"reduction dtc {100 * red['dtc']:.1f}% dtvs {100 * red['dtvs']:.1f}%", flush=True)
