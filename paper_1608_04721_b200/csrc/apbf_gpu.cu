@@ -26,6 +26,17 @@ static constexpr int kAabbBlock = APBF_AABB_BLOCK;
 
 #include <memory>
 #include <functional>
+
+#include <nvtx3/nvToolsExt.h>
+
+// NVTX ranges around the host-side phases (frames, slab substeps), for
+// Nsight Systems timelines.
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange&) = delete;
+    NvtxRange& operator=(const NvtxRange&) = delete;
+};
 #include <thread>
 
 using namespace apbf_gpu;
@@ -117,7 +128,13 @@ struct DBuf {
     void ensure(size_t m) {
         if (m <= n && p) return;
         release();
-        CK(cudaMalloc(&p, sizeof(T) * std::max<size_t>(m, 1) + kBufSlack));
+        const size_t bytes = sizeof(T) * std::max<size_t>(m, 1) + kBufSlack;
+        CK(cudaMalloc(&p, bytes));
+        // zeroed once: the scans' read-ahead past a run or list end (tail
+        // slack, kListPad rows) then reads defined, unused values
+        // (compute-sanitizer --tool initcheck stays clean)
+        CK(cudaMemsetAsync(p, 0, bytes, 0));
+        CK(cudaStreamSynchronize(0));
         n = std::max<size_t>(m, 1);
         ++g_alloc_gen;
     }
@@ -1152,6 +1169,7 @@ struct apbf_gpu_solver {
 
     void frame(bool assign_lod, const apbf_camera* cam, const apbf_lod_config* lod, int frame_index,
                apbf_frame_stats* out) {
+        NvtxRange range(transport ? "apbf slab frame" : "apbf frame");
         CK(cudaSetDevice(ws.device));
         if (transport) {
             if (post_pass()) fail(APBF_ERR_INVALID_ARGUMENT, "the velocity post-pass runs on one rank");
@@ -1531,6 +1549,7 @@ struct apbf_gpu_solver {
         }
         tmark("lod");
         for (int s = 0; s < cfg.substeps; ++s) {
+            NvtxRange range("apbf slab substep");
             localPre[s] = n;
             StateSet src = set[cur].view(), dst = set[cur ^ 1].view();
             KL(k_substep_reset<<<1, 1, 0, st>>>(ctl));
