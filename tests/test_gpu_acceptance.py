@@ -35,17 +35,20 @@ def test_criterion_2_3_density_tracks_pbf_and_adaptivity_cuts_work():
 
 
 def test_criterion_3_wall_clock_reduction_at_1m():
-    """C3 (time part): APBF's median frame time is below PBF at N_max -- on the
-    BASELINE 1M ocean, APBF {5..10} vs PBF 10.  The reference's bar (>= 15% at
-    27k particles on its CPU) does not transfer: on the B200 a 27k frame is
-    launch-bound, and at 1M the per-frame fixed cost (grid, lists, LOD, ~0.75
-    ms) dilutes the 24% work cut to a ~15% time cut (profiles/README.md, C4
-    sweep: 18.2% reduction at N = 20).  Asserted here with margin: >= 5%."""
+    """C3 (time part), with the reference's own bar and protocol
+    (acceptance_main.cpp:145-153): runBench over 80 frames -- "the settled
+    regime where constraint work dominates the fixed per-frame costs" -- and
+    a median-frame reduction (t_pbf - t_apbf) / t_pbf >= 15% for DTVS or DTC.
+    On the BASELINE 1M ocean, APBF {5..10} vs PBF 10 (a 27k frame is
+    launch-bound on a B200).  Measured: DTC 15.8%, DTVS 13.2%
+    (profiles/README.md); the remaining gap to the 24% iteration cut is the
+    per-frame fixed cost (grid, lists, LOD)."""
     spec = S.build_scenario("ocean_1m")
-    res = H.run_bench(spec, H.parse_bench_modes("pbf:10,apbf:dtc,apbf:dtvs"), 3, 10, 1)
+    res = H.run_bench(spec, H.parse_bench_modes("pbf:10,apbf:dtvs,apbf:dtc"), 1, 80, 1)
     t_pbf = res[0].median_frame_ms
     red = [(t_pbf - r.median_frame_ms) / t_pbf for r in res[1:]]
-    assert max(red) >= 0.05, (H.format_bench_report(res), red)
+    assert red[0] >= 0.15 or red[1] >= 0.15, (H.format_bench_report(res), red)
+    assert min(red) > 0.08, red  # both modes cut the frame
 
 
 def test_criterion_4_residual_decreases_over_iterations():
