@@ -29,9 +29,19 @@ def _stale(out, deps) -> bool:
     return any(os.path.getmtime(d) > t for d in deps if os.path.exists(d))
 
 
-def build_cuda(force: bool = False) -> str:
+CHECKED = os.path.join(HERE, "libapbf_gpu_checked.so")
+
+
+def build_cuda(force: bool = False, checked: bool = True) -> str:
+    """libapbf_gpu.so (the product) and libapbf_gpu_checked.so: the same code
+    with -DAPBF_CHECKED device asserts on every data-derived index (selected
+    with APBF_LIB=libapbf_gpu_checked.so; tools/checked_run.sh)."""
     if force or _stale(OUT, DEPS):
         cmd = [NVCC, *FLAGS, "-o", OUT, *SOURCES]
+        print("[build]", " ".join(cmd), flush=True)
+        subprocess.run(cmd, check=True)
+    if checked and (force or _stale(CHECKED, DEPS)):
+        cmd = [NVCC, *FLAGS, "-DAPBF_CHECKED", "-o", CHECKED, *SOURCES]
         print("[build]", " ".join(cmd), flush=True)
         subprocess.run(cmd, check=True)
     return OUT
