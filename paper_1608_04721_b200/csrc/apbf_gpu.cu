@@ -314,8 +314,8 @@ void validate_lod(const apbf_lod_config& l) {
 // LOD on device for positions X (float4): levels into LV.
 // lodDtc (lod.hpp:83-104) / lodDtvs (lod.hpp:109-156).
 void run_lod(Workspace& ws, const float4* X, int n, const apbf_camera& cam, const apbf_lod_config& lod,
-             float radius, int* LV) {
-    cudaStream_t st = ws.stream;
+             float radius, int* LV, cudaStream_t on = nullptr) {
+    cudaStream_t st = on ? on : ws.stream;
     ws.dist.ensure(n);
     ws.keys.ensure(n);
     const bool dtvs = lod.model == APBF_LOD_DTVS;
@@ -469,6 +469,9 @@ struct apbf_gpu_solver {
         cap = cfg.velocity_cap > 0.0f ? cfg.velocity_cap : cfg.h / dt;
         S = cfg.stab_threshold > 0 ? cfg.stab_threshold : cfg.n_max;
         for (auto& e : ev) CK(cudaEventCreate(&e));
+        CK(cudaStreamCreateWithFlags(&lod_stream, cudaStreamNonBlocking));
+        CK(cudaEventCreateWithFlags(&ev_lod_fork, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&ev_lod_join, cudaEventDisableTiming));
         const unsigned evf = std::getenv("APBF_E2E_TRACE") ? cudaEventDefault : cudaEventDisableTiming;
         CK(cudaEventCreateWithFlags(&ev_x, evf));
         CK(cudaEventCreateWithFlags(&ev_inputs, evf));
@@ -490,6 +493,9 @@ struct apbf_gpu_solver {
         if (ev_inputs) cudaEventDestroy(ev_inputs);
         if (copy_stream) cudaStreamDestroy(copy_stream);
         if (comm_stream) cudaStreamDestroy(comm_stream);
+        if (lod_stream) cudaStreamDestroy(lod_stream);
+        if (ev_lod_fork) cudaEventDestroy(ev_lod_fork);
+        if (ev_lod_join) cudaEventDestroy(ev_lod_join);
         if (ev_halo_ready) cudaEventDestroy(ev_halo_ready);
         if (ev_halo_done) cudaEventDestroy(ev_halo_done);
     }
@@ -790,6 +796,12 @@ struct apbf_gpu_solver {
         kt_used = 0;
         n_iter = n;
         KL(k_frame_begin<<<1, 1, 0, st>>>(ctl));
+        // The LOD pass (APBF) reads only x and writes only the levels and its
+        // own control fields; nothing before the first reorder reads levels.
+        // So it forks onto lod_stream and runs beside the first substep's
+        // predict and grid build (graph branches), joined before k_gather.
+        // (Serial under phase timing or an observer.)
+        bool lod_forked = false;
         if (assign_lod) {
             if (cfg.mode == APBF_MODE_PBF) {
                 KL(k_fill_int<<<blocks(n, 256), 256, 0, st>>>(set[cur].LV.p, n, nMax));
@@ -797,7 +809,15 @@ struct apbf_gpu_solver {
                 apbf_lod_config lc = *lod;
                 lc.n_min = cfg.n_min;
                 lc.n_max = cfg.n_max;
-                run_lod(ws, set[cur].X.p, n, *cam, lc, radius, set[cur].LV.p);
+                lod_forked = !phase_timing && !observer;
+                if (lod_forked) {
+                    CK(cudaEventRecord(ev_lod_fork, st));
+                    CK(cudaStreamWaitEvent(lod_stream, ev_lod_fork, 0));
+                    run_lod(ws, set[cur].X.p, n, *cam, lc, radius, set[cur].LV.p, lod_stream);
+                    CK(cudaEventRecord(ev_lod_join, lod_stream));
+                } else {
+                    run_lod(ws, set[cur].X.p, n, *cam, lc, radius, set[cur].LV.p);
+                }
             }
         }
         mark(1);
@@ -827,6 +847,7 @@ struct apbf_gpu_solver {
                 if (capturing) CK(cudaStreamWaitEvent(st, ev_inputs, cudaEventWaitExternal));
                 else CK(cudaStreamWaitEvent(st, ev_inputs, 0));
             }
+            if (s == 0 && lod_forked) CK(cudaStreamWaitEvent(st, ev_lod_join, 0));  // levels ready
             KL(k_gather<<<numTiles, kTileThreads, smemG, st>>>(n, ctl, ws.perm.p, pin, dst, nMax, numTiles,
                                                            tileCount.p));
             if (s == cfg.substeps - 1) rec(ev[7]);  // final storage order (overlapped download)
@@ -1447,6 +1468,8 @@ struct apbf_gpu_solver {
     }
 
     cudaStream_t comm_stream = nullptr;  // slab mode: the x* halo exchange (overlapped)
+    cudaStream_t lod_stream = nullptr;   // the frame's LOD pass, beside the first predict + grid
+    cudaEvent_t ev_lod_fork = nullptr, ev_lod_join = nullptr;
     cudaEvent_t ev_halo_ready = nullptr, ev_halo_done = nullptr;
 
     // APBF_SLAB_TRACE=1: host enqueue time vs device time of the slab frame's
