@@ -240,9 +240,12 @@ struct alignas(64) Rec {
     int pad[3];
 };
 
-__global__ void k_pack_recs(int cnt, const int* __restrict__ idx, StateSet s, Rec* __restrict__ out) {
+// Records [0, cnt) except the rank's own segment [skipB, skipE), which
+// never leaves the device (k_gather_self).
+__global__ void k_pack_recs(int cnt, const int* __restrict__ idx, StateSet s, Rec* __restrict__ out,
+                            int skipB = 0, int skipE = 0) {
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
-    if (k >= cnt) return;
+    if (k >= cnt || (k >= skipB && k < skipE)) return;
     const int i = idx[k];
     const float4 x = s.X[i], v = s.V[i], xs = s.XS[i];
     Rec r;
@@ -263,9 +266,9 @@ __global__ void k_pack_recs(int cnt, const int* __restrict__ idx, StateSet s, Re
     out[k] = r;
 }
 
-__global__ void k_unpack_recs(int cnt, const Rec* __restrict__ in, StateSet d) {
+__global__ void k_unpack_recs(int cnt, const Rec* __restrict__ in, StateSet d, int skipB = 0, int skipE = 0) {
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
-    if (k >= cnt) return;
+    if (k >= cnt || (k >= skipB && k < skipE)) return;
     const Rec r = in[k];
     d.X[k] = make_float4(r.x[0], r.x[1], r.x[2], 0.f);
     d.V[k] = make_float4(r.v[0], r.v[1], r.v[2], 0.f);
@@ -273,6 +276,20 @@ __global__ void k_unpack_recs(int cnt, const Rec* __restrict__ in, StateSet d) {
     d.W[k] = r.w;
     d.L[k] = r.lam;
     d.LV[k] = r.lv;
+}
+
+// The particles a rank keeps (its own exchange segment): straight from the
+// old state into their slots of the new local set, no record round trip.
+__global__ void k_gather_self(int m, const int* __restrict__ idx, StateSet from, StateSet to, int off) {
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= m) return;
+    const int i = idx[k];
+    to.X[off + k] = from.X[i];
+    to.V[off + k] = from.V[i];
+    to.XS[off + k] = from.XS[i];
+    to.W[off + k] = from.W[i];
+    to.L[off + k] = from.L[i];
+    to.LV[off + k] = from.LV[i];
 }
 
 // One all-reduce instead of three for the substep's grid: [~abort, lo(3),

@@ -1633,8 +1633,12 @@ struct apbf_gpu_solver {
             KL(k_dest_starts<<<1, 32, 0, st>>>(destCountD.p, G, destStartD.p));
             KL(k_mask_scatter<<<tiles, kTileThreads, 0, st>>>(n, destMask.p, G, tiles, destTile.p, destStartD.p,
                                                             sendIdx.p));
-            if (nsend > 0)
-                KL(k_pack_recs<<<blocks(nsend, 256), 256, 0, st>>>((int)nsend, sendIdx.p, src, sendRec.p));
+            // records only for the other ranks; this rank's own segment goes
+            // straight from the old state (src) into the new local set (dst)
+            const int selfB = (int)sendStart[g], selfE = (int)(sendStart[g] + sendCnt[g]);
+            if (nsend > sendCnt[g])
+                KL(k_pack_recs<<<blocks(nsend, 256), 256, 0, st>>>((int)nsend, sendIdx.p, src, sendRec.p, selfB,
+                                                                 selfE));
             std::vector<const void*> sp(G);
             std::vector<void*> rp(G);
             std::vector<size_t> sb(G), rb(G);
@@ -1644,12 +1648,17 @@ struct apbf_gpu_solver {
                 rp[q] = recvRec.p + roff[q];
                 rb[q] = sizeof(Rec) * recvCnt[q];
             }
-            if (sendCnt[g])
-                CK(cudaMemcpyAsync(recvRec.p + roff[g], sendRec.p + sendStart[g], sizeof(Rec) * sendCnt[g],
-                                   cudaMemcpyDeviceToDevice, st));
             T.alltoallv(sp.data(), sb.data(), rp.data(), rb.data(), st);
             const int nL = (int)nLocal;
-            KL(k_unpack_recs<<<blocks(nL, 256), 256, 0, st>>>(nL, recvRec.p, src));
+            if (sendCnt[g])
+                KL(k_gather_self<<<blocks(sendCnt[g], 256), 256, 0, st>>>((int)sendCnt[g], sendIdx.p + selfB, src,
+                                                                        dst, (int)roff[g]));
+            if (nL > sendCnt[g])
+                KL(k_unpack_recs<<<blocks(nL, 256), 256, 0, st>>>(nL, recvRec.p, dst, (int)roff[g],
+                                                                (int)(roff[g] + sendCnt[g])));
+            // the new local set is dst; the old state set is free and becomes the
+            // sorted set the iterations run on
+            std::swap(src, dst);
             tmark("exchange");
             // local stable sort by global cell == global order restricted
             ws.run_grid(0, src.XS, nL, cfg.h, cfg.h, false, radius);
@@ -1763,6 +1772,7 @@ struct apbf_gpu_solver {
             if (nOwn > 0) KL(k_copy_owned<<<blocks(nOwn, 256), 256, 0, st>>>(nOwn, ownB, dst, src));
             n = nOwn;
             localPost[s] = n;
+            cur ^= 1;  // the owned state now lives in the other set (src after the swap)
             tmark("finalize+copy");
         }
         CK(cudaEventRecord(ev[5], st));
@@ -1897,6 +1907,14 @@ struct apbf_gpu_solver {
                 if (layers) layer_cap = std::max(2 * layer_cap, ws.h_ctl->need_layers + 16);
             }
             const Ctl& c = *ws.h_ctl;
+            if (c.abort || c.runtime_error || c.slab_error) {
+                // all-or-nothing, as on one GPU: the rank's frame-start state
+                // from the backup set (levels as before the frame's LOD)
+                cur = start_set;
+                n = start_n;
+                copy_set(set[cur], set[2]);
+                CK(cudaStreamSynchronize(ws.stream));
+            }
             if (c.runtime_error) fail(APBF_ERR_RUNTIME, "grid cell count exceeds limit; domain blew up");
             if (c.slab_error) fail(APBF_ERR_RUNTIME, "too few grid layers for the slab decomposition");
             // global first error: (substep, iteration, pass, global index) -- only

@@ -111,3 +111,20 @@ def test_nccl_transport_single_rank_matches_plain_solver():
     nc.download(b)
     for k in FIELDS:
         assert np.array_equal(getattr(a, k), getattr(b, k)), k
+
+
+def test_failed_slab_frame_keeps_start_state():
+    """All-or-nothing across ranks too: after a failing slab frame (NaN in one
+    rank's slice, found in predict) every rank holds its frame-start state,
+    so the group downloads the input unchanged."""
+    spec = S.build_scenario("dam_break", 8000 / 216000)
+    spec.solver.range = IterationRange(3, 5)
+    st = S.make_state(spec, 2)
+    st.level[:] = 4
+    st.v[6000, 2] = np.nan
+    before = st.copy()
+    grp = SlabGroup(spec.solver, spec.scene, nranks=2, devices=[0, 0])
+    with pytest.raises(NumericalError):
+        grp.step_frame_with_levels(st, 0)
+    for k in FIELDS:
+        assert np.array_equal(getattr(st, k), getattr(before, k), equal_nan=True), k
