@@ -109,6 +109,10 @@ public:
     const SolverConfig<Scalar>& config() const { return cfg_; }
     const SdfScene<Scalar>& scene() const { return scene_; }
 
+    // The fast build of the lambda / delta-p pair arithmetic (apbf_gpu_set_fast_math):
+    // outside the bitwise contract, within the tier-B tolerance of Solver<double>.
+    void setFastMath(bool on) { apbf_gpu_set_fast_math(h_, on ? 1 : 0); }
+
     // Called after every iteration's position application with the substep
     // index, the 1-based iteration and the current state (solver.hpp:222-224).
     std::function<void(int, int, const ParticleSet<Scalar>&)> iterationObserver;
