@@ -19,8 +19,12 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--fast", action="store_true")
 ap.add_argument("--warm", type=int, default=3)
 ap.add_argument("--scenario", default="ocean_1m")
+ap.add_argument("--lod", default=None, choices=[None, "dtc", "dtvs"])
 a = ap.parse_args()
 spec = S.build_scenario(a.scenario)
+if a.lod:
+    from paper_1608_04721_b200 import LodModel
+    spec.lod.model = LodModel.DTC if a.lod == "dtc" else LodModel.DTVS
 sv = Solver(spec.solver, spec.scene)
 sv.set_fast_math(a.fast)
 sv.upload(S.make_state(spec, 1))
