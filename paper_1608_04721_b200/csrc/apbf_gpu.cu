@@ -334,9 +334,8 @@ void run_lod(Workspace& ws, const float4* X, int n, const apbf_camera& cam, cons
                                                    ws.keys.p));
     }
     if (lod.auto_range) {
-        KL(k_rs_init<<<1, 1, 0, st>>>(ws.rs.p, ws.ctl.p, n, dtvs ? 1 : 0));
-        KL(k_rs_clear<<<1, 1024, 0, st>>>(ws.rs.p));
-        const int hb = std::min(blocks(n, 256), 2 * 148);
+        KL(k_rs_init<<<1, 1024, 0, st>>>(ws.rs.p, ws.ctl.p, n, dtvs ? 1 : 0));
+        const int hb = std::min(blocks(n, 256), 16 * 148);  // ~2 keys per thread: no load chain
         for (int pass = 0; pass < 3; ++pass) {
             KL(k_rs_hist<<<hb, 256, 0, st>>>(n, ws.keys.p, ws.rs.p, pass));
             KL(k_rs_select<<<1, 1024, 0, st>>>(ws.rs.p, pass));
@@ -1452,9 +1451,8 @@ struct apbf_gpu_solver {
                                                          ws.dist.p, ws.keys.p));
         }
         if (lod.auto_range) {
-            KL(k_rs_init<<<1, 1, 0, st>>>(ws.rs.p, ws.ctl.p, (int)nAll, dtvs ? 1 : 0));
-            KL(k_rs_clear<<<1, 1024, 0, st>>>(ws.rs.p));
-            const int hb = std::min(blocks(nn, 256), 2 * 148);
+            KL(k_rs_init<<<1, 1024, 0, st>>>(ws.rs.p, ws.ctl.p, (int)nAll, dtvs ? 1 : 0));
+            const int hb = std::min(blocks(nn, 256), 16 * 148);
             for (int pass = 0; pass < 3; ++pass) {
                 KL(k_rs_hist<<<hb, 256, 0, st>>>(nn, ws.keys.p, ws.rs.p, pass));
                 T.allreduce(&ws.rs.p->hist[0][0], 4 * 2048, RType::U32, ROp::Sum, st);
