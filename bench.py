@@ -139,6 +139,17 @@ def ncu_kernel(kernel: str):
         return None, None
 
 
+def ncu_warp_instructions(kernel: str):
+    """Warp instructions of the committed full-activity ncu launch of `kernel`
+    (iteration 1 of a 1M-particle frame: 1,000,000 particle-iterations), or None."""
+    path = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    try:
+        with open(path) as f:
+            return float(json.load(f)["kernels"][kernel]["smsp__inst_executed.sum"].split()[0])
+    except Exception:
+        return None
+
+
 def bench_scenario(args, world):
     """C3 (1M ocean) on one GPU; C5 (8M tank, strong scaling) on N > 1."""
     return args.scenario if world == 1 else "tank_8m"
@@ -230,6 +241,20 @@ def rooflines(kt, ms_kt, nbar, sm_mhz, hbm_peak, peak_kind, steps, fma):
               "unit": "TFLOP/s", "frac": fp32_achieved / fp32_peak, "nbar": nbar,
               "flops_per_particle_iteration": flops_pi,
               "peak_note": "148 SMs x 128 lanes x median SM clock" + (" x 2 (FMA)" if fma else ", no FMA credit")}
+    # the bound that actually binds these passes: instruction issue (ncu:
+    # 68-80% issue-active in the parity build), warp instructions per
+    # particle-iteration from the committed full-activity ncu launch
+    winst = ncu_warp_instructions(f"k_{dom}" + ("_fast" if fma else ""))
+    if winst:
+        inst_pi = winst / 1e6
+        issue_peak = 148 * 4 * sm_mhz * 1e6 / 1e9  # G warp-instructions/s: 4 schedulers per SM
+        issue_achieved = inst_pi * pis_per_launch / (per_launch_ms / 1e3) / 1e9
+        roof32["issue"] = {"bound": "issue", "achieved": issue_achieved, "peak": issue_peak,
+                           "unit": "G warp-instructions/s", "frac": issue_achieved / issue_peak,
+                           "warp_instructions_per_particle_iteration": inst_pi,
+                           "note": "instructions per particle-iteration from the ncu --set full launch "
+                                   "(iteration 1, 1M particle-iterations); time from the CUDA-event "
+                                   "average launch, late partly-active iterations included"}
     return roof, roof32
 
 
