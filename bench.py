@@ -475,7 +475,7 @@ def run_ours(args, world, rank, local, pg):
         if world > 1:
             host = slice_state(host, rank, world)
         n_host = host.count()
-        cap = n_host if world == 1 else 2 * n_global // world + 4096
+        cap = n_host if world == 1 else n_global + 4096  # a rank never holds more than all particles
 
         def pinned(shape, dtype):
             return torch.empty(shape, dtype=dtype, pin_memory=True).numpy()

@@ -1322,6 +1322,7 @@ struct apbf_gpu_solver {
 
     Transport* transport = nullptr;
     long long n_global_ = 0;  // slab mode: particles over all ranks (set_state_local)
+    long long send_capacity = 0;  // slab mode: exchange send buffers (set_state_local)
     std::unique_ptr<Transport> transport_owned;
     long long n_capacity = 0;
     DBuf<int> layerHist, zRange, bounds, destTile, destCountD, destStartD, sendIdx, LVo, ownedFlag,
@@ -1361,19 +1362,27 @@ struct apbf_gpu_solver {
     void set_state_local(int nloc, long long ntotal, const float* x, const float* xs, const float* v,
                          const float* mass, const float* inv_mass, const float* lambda,
                          const int32_t* level) {
-        // owned + ghost copies: a rank can hold more than n_global / G, and
-        // the sends of one rank (owned + ghost duplicates) more than n_global
-        n_capacity = 2 * std::max<long long>(ntotal, 1) + 4096;
+        // Capacities that no input can exceed, so that no rank ever has to
+        // fail on its own between collectives:
+        // * a rank receives every particle at most once: local (owned +
+        //   ghost) counts <= n_global;
+        // * a substep sends each particle to at most 3 ranks (its owner and
+        //   the two neighbours whose 2-layer halo it may sit in; slabs are
+        //   >= 2 layers thick), the metrics exchange to at most G.
+        const int G = transport ? transport->size() : 1;
+        const long long nt = std::max<long long>(ntotal, 1);
+        n_capacity = nt + 4096;
         n_global_ = ntotal;
+        send_capacity = (long long)std::max(3, G) * nt + 4096;
         allocate((int)n_capacity);
         destMask.ensure(n_capacity);
-        sendIdx.ensure(n_capacity);
+        sendIdx.ensure(send_capacity);
         LVo.ensure(n_capacity);
         ownedFlag.ensure(n_capacity);
         ownedSorted.ensure(n_capacity);
-        sendRec.ensure(n_capacity);
+        sendRec.ensure(3 * nt + 4096);
         recvRec.ensure(n_capacity);
-        sendPM.ensure(n_capacity);
+        sendPM.ensure(send_capacity);
         recvPM.ensure(n_capacity);
         zRange.ensure(2 * kMaxRanks);
         bounds.ensure(8);
@@ -1617,10 +1626,10 @@ struct apbf_gpu_solver {
                 hiG0 += c[7];    // layer hi
                 hiG1 += c[8];    // layer hi+1
             }
-            // a rank receives every particle at most once: nLocal <= nAll <=
-            // n_capacity always; the send side was checked on the device
-            if (nLocal > n_capacity || nsend > n_capacity)
-                fail(APBF_ERR_RUNTIME, "slab exchange exceeds the per-rank capacity");
+            // cannot happen (set_state_local sizes for the worst case); an
+            // internal error, not an input condition
+            if (nLocal > n_capacity || nsend > 3 * std::max<long long>(n_global_, 1) + 4096)
+                fail(APBF_ERR_RUNTIME, "internal: slab exchange larger than its worst-case capacity");
             const int ownB = (int)(lowG0 + lowG1), l1B = (int)lowG0;
             const int ownE = (int)(nLocal - hiG0 - hiG1), l1E = (int)(nLocal - hiG1);
             const int lowEnd = (int)(ownB + own2lo), highB = (int)(ownE - ownHi2);
@@ -1824,8 +1833,8 @@ struct apbf_gpu_solver {
             roff[q] = nM;
             nM += recvCnt[q];
         }
-        if (nM > n_capacity || nsend > n_capacity)
-            fail(APBF_ERR_RUNTIME, "slab metrics exchange exceeds the per-rank capacity");
+        if (nM > n_capacity || nsend > send_capacity)  // cannot happen: see set_state_local
+            fail(APBF_ERR_RUNTIME, "internal: slab metrics exchange larger than its worst-case capacity");
         const int tiles = std::max(1, (n + kTileSize - 1) / kTileSize);
         destTile.ensure((size_t)G * tiles);
         KL(k_mask_tile_counts<<<tiles, kTileThreads, 0, st>>>(n, destMask.p, G, tiles, destTile.p));
