@@ -168,6 +168,8 @@ struct Workspace {
     DBuf<Scene> scene;
     DBuf<RadixSel> rs;
     DBuf<int> depth;
+    DBuf<float4> rays;  // per-pixel ray direction + |d|^2 (k_splat_prep)
+    DBuf<float> raysa;  // per-pixel sqrt(|d|^2)
     DBuf<float> dist;
     DBuf<unsigned> keys;
     DBuf<float4> tmp4;
@@ -323,8 +325,10 @@ void run_lod(Workspace& ws, const float4* X, int n, const apbf_camera& cam, cons
         const CamFrame f = make_frame(cam);
         const size_t px = (size_t)cam.width * cam.height;
         ws.depth.ensure(px);
-        KL(k_fill_int<<<blocks((long long)px, 256), 256, 0, st>>>(ws.depth.p, (int)px, 0x7f800000));
-        KL(k_splat<<<blocks(n, 256), 256, 0, st>>>(n, X, radius, f, ws.depth.p));
+        ws.rays.ensure(px);
+        ws.raysa.ensure(px);
+        KL(k_splat_prep<<<blocks((long long)px, 256), 256, 0, st>>>(f, ws.depth.p, ws.rays.p, ws.raysa.p));
+        KL(k_splat<<<blocks(n, 256), 256, 0, st>>>(n, X, radius, f, ws.depth.p, ws.rays.p, ws.raysa.p));
         // each LOD pass counts its own visible sample (several per frame with cameras)
         CK(cudaMemsetAsync(&ws.ctl.p->sample_count, 0, sizeof(int), st));
         KL(k_dtvs_gap<<<blocks(n, 256), 256, 0, st>>>(n, X, radius, f, ws.depth.p, ws.dist.p, ws.keys.p,
@@ -846,9 +850,17 @@ struct apbf_gpu_solver {
                 if (capturing) CK(cudaStreamWaitEvent(st, ev_inputs, cudaEventWaitExternal));
                 else CK(cudaStreamWaitEvent(st, ev_inputs, 0));
             }
-            if (s == 0 && lod_forked) CK(cudaStreamWaitEvent(st, ev_lod_join, 0));  // levels ready
-            KL(k_gather<<<numTiles, kTileThreads, smemG, st>>>(n, ctl, ws.perm.p, pin, dst, nMax, numTiles,
-                                                           tileCount.p));
+            if (s == 0 && lod_forked) {
+                // the fields now, the levels once the forked LOD pass joins
+                KL(k_gather<<<numTiles, kTileThreads, smemG, st>>>(n, ctl, ws.perm.p, pin, dst, nMax, numTiles,
+                                                               tileCount.p, 1));
+                CK(cudaStreamWaitEvent(st, ev_lod_join, 0));
+                KL(k_gather<<<numTiles, kTileThreads, smemG, st>>>(n, ctl, ws.perm.p, pin, dst, nMax, numTiles,
+                                                               tileCount.p, 2));
+            } else {
+                KL(k_gather<<<numTiles, kTileThreads, smemG, st>>>(n, ctl, ws.perm.p, pin, dst, nMax, numTiles,
+                                                               tileCount.p));
+            }
             if (s == cfg.substeps - 1) rec(ev[7]);  // final storage order (overlapped download)
             KL(k_level_scan<<<nMax + 1, 1024, 0, st>>>(ctl, numTiles, tileCount.p, levelCount.p));
             KL(k_level_finish<<<1, 32, 0, st>>>(ctl, n, nMax, levelCount.p, activeCount.p, bucketStart.p));
@@ -1449,8 +1461,10 @@ struct apbf_gpu_solver {
             const CamFrame f = make_frame(cam);
             const size_t px = (size_t)cam.width * cam.height;
             ws.depth.ensure(px);
-            KL(k_fill_int<<<blocks((long long)px, 256), 256, 0, st>>>(ws.depth.p, (int)px, 0x7f800000));
-            KL(k_splat<<<blocks(nn, 256), 256, 0, st>>>(nn, X, radius, f, ws.depth.p));
+            ws.rays.ensure(px);
+            ws.raysa.ensure(px);
+            KL(k_splat_prep<<<blocks((long long)px, 256), 256, 0, st>>>(f, ws.depth.p, ws.rays.p, ws.raysa.p));
+            KL(k_splat<<<blocks(nn, 256), 256, 0, st>>>(nn, X, radius, f, ws.depth.p, ws.rays.p, ws.raysa.p));
             T.allreduce(ws.depth.p, px, RType::I32, ROp::Min, st);  // positive float bits: int order
             KL(k_dtvs_gap<<<blocks(nn, 256), 256, 0, st>>>(nn, X, radius, f, ws.depth.p, ws.dist.p,
                                                          ws.keys.p, ws.ctl.p));
@@ -2525,10 +2539,13 @@ int32_t apbf_gpu_splat(int32_t n, const float* positions, float radius, const ap
         Workspace& ws = component_ws();
         const size_t px = (size_t)cam->width * cam->height;
         ws.depth.ensure(px);
-        KL(k_fill_int<<<blocks((long long)px, 256), 256, 0, ws.stream>>>(ws.depth.p, (int)px, 0x7f800000));
+        ws.rays.ensure(px);
+        ws.raysa.ensure(px);
+        KL(k_splat_prep<<<blocks((long long)px, 256), 256, 0, ws.stream>>>(f, ws.depth.p, ws.rays.p, ws.raysa.p));
         if (n > 0) {
             upload_pos4(ws, n, positions);
-            KL(k_splat<<<blocks(n, 256), 256, 0, ws.stream>>>(n, ws.tmp4.p, radius, f, ws.depth.p));
+            KL(k_splat<<<blocks(n, 256), 256, 0, ws.stream>>>(n, ws.tmp4.p, radius, f, ws.depth.p, ws.rays.p,
+                                                           ws.raysa.p));
         }
         LAUNCH_CHECK();
         CK(cudaMemcpyAsync(depth_out, ws.depth.p, sizeof(float) * px, cudaMemcpyDeviceToHost, ws.stream));
