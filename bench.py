@@ -378,10 +378,18 @@ def run_ours(args, world, rank, local, pg):
     torch.cuda.synchronize()
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
+    # per-frame events between the frames (the median frame, and
+    # the frame without the metrics pass = FrameStats.wallMs, the reference's)
+    fev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
     e0.record(ext)
+    fev[0].record(ext)
     its = 0
+    wall = []
     for f in range(args.steps):
-        its += solver.step_frame_resident(cam, lod, 1000 + f).total_iterations  # global total
+        st_f = solver.step_frame_resident(cam, lod, 1000 + f)
+        its += st_f.total_iterations  # global total
+        wall.append(st_f.wall_ms)
+        fev[f + 1].record(ext)
     e1.record(ext)
     e1.synchronize()
     torch.cuda.synchronize()
@@ -389,6 +397,7 @@ def run_ours(args, world, rank, local, pg):
     clk = clocks.stop()
     launches = Solver.launch_count() - launches0
     ms = e0.elapsed_time(e1)
+    frame_ms = [fev[f].elapsed_time(fev[f + 1]) for f in range(args.steps)]
     entries, _ = solver.last_neighbor_stats()
 
     # ------- instrumented twin region: per-launch events on the solver passes -------
@@ -548,6 +557,9 @@ def run_ours(args, world, rank, local, pg):
         "dtype": "f32", "data": "synthetic",
         "config": make_config(spec, world, args),
         "steps_per_s": args.steps / (ms_max / 1e3),
+        "median_ms_per_step": statistics.median(frame_ms),
+        "ms_per_step_no_metrics": statistics.mean(wall),
+        "substeps_per_s": spec.solver.substeps * args.steps / (ms_max / 1e3),
         "particle_iterations_per_step": its / args.steps,
         "e2e": e2e,
         "gpu_launches": launches,
