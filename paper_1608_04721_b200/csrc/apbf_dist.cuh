@@ -29,33 +29,83 @@ __device__ __forceinline__ int layer_of(const GridDev& G, float h, float z) {
 // histogram holds `cap` layers (a device-sized grid): a deeper grid flags
 // need_layers and aborts the frame (identically on every rank: the grid is
 // global), and the host grows the histogram and runs the frame again.
-__global__ void k_layer_hist(int n, const float4* __restrict__ P, const int* __restrict__ LV,
-                             Ctl* ctl, int g, float h, int* __restrict__ hist, int cap) {
+//
+// Each CTA takes one contiguous range of the storage order (cell order, so
+// the range spans few layers) and aggregates in shared memory over a window
+// of kHistWin layers from the range's first one; global atomics then go one
+// per (CTA, layer) -- per warp they serialise at L2 on the few bins (about
+// 600 per bin at 1M particles and 50 layers: 25 us).
+constexpr int kHistItems = 4;
+constexpr int kHistWin = 64;
+__global__ void __launch_bounds__(256) k_layer_hist(int n, const float4* __restrict__ P, const int* __restrict__ LV,
+                                                    Ctl* ctl, int g, float h, int* __restrict__ hist, int cap) {
+    __shared__ int s_h[kHistWin];
+    __shared__ int s_key0;
     if (ctl->abort) return;
-    if (ctl->grid[g].dims[2] > cap) {
+    const GridDev G = ctl->grid[g];
+    if (G.dims[2] > cap) {
         if (blockIdx.x == 0 && threadIdx.x == 0) {
-            ctl->need_layers = ctl->grid[g].dims[2];
+            ctl->need_layers = G.dims[2];
             ctl->abort = 1;
         }
         return;
     }
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    // storage order is cell order, so a warp's particles share few layers:
-    // one atomic per distinct layer of the warp (match + reduce), not per particle
-    const int key = i < n ? layer_of(ctl->grid[g], h, P[i].z) : -1;
-    const int val = i < n ? 1 + LV[i] : 0;
-    const unsigned same = __match_any_sync(0xffffffffu, key);
-    const int sum = __reduce_add_sync(same, val);
-    if (key >= 0 && (threadIdx.x & 31) == __ffs(same) - 1) atomicAdd(&hist[key], sum);
+    const int per = (n + gridDim.x - 1) / gridDim.x;
+    const int b0 = blockIdx.x * per, b1 = imin_std(n, b0 + per);
+    for (int t = threadIdx.x; t < kHistWin; t += blockDim.x) s_h[t] = 0;
+    if (threadIdx.x == 0) s_key0 = b0 < n ? layer_of(G, h, P[b0].z) : 0;
+    __syncthreads();
+    const int key0 = s_key0;
+    for (int base = b0; base < b1; base += kHistItems * blockDim.x) {
+        float z[kHistItems];
+        int lv[kHistItems];
+#pragma unroll
+        for (int j = 0; j < kHistItems; ++j) {  // the chunk's loads issued together
+            const int i = base + j * blockDim.x + threadIdx.x;
+            z[j] = i < b1 ? P[i].z : 0.f;
+            lv[j] = i < b1 ? LV[i] : 0;
+        }
+#pragma unroll
+        for (int j = 0; j < kHistItems; ++j) {
+            const int i = base + j * blockDim.x + threadIdx.x;
+            // one shared atomic per distinct layer of the warp (a warp inside
+            // one layer -- nearly all of them -- skips the match)
+            const int key = i < b1 ? layer_of(G, h, z[j]) : -1;
+            const int val = i < b1 ? 1 + lv[j] : 0;
+            const unsigned same = __all_sync(0xffffffffu, key == __shfl_sync(0xffffffffu, key, 0))
+                                      ? 0xffffffffu
+                                      : __match_any_sync(0xffffffffu, key);
+            const int sum = __reduce_add_sync(same, val);
+            if (key >= 0 && (threadIdx.x & 31) == __ffs(same) - 1) {
+                const int d = key - key0;
+                if (d >= 0 && d < kHistWin) atomicAdd(&s_h[d], sum);
+                else atomicAdd(&hist[key], sum);
+            }
+        }
+    }
+    __syncthreads();
+    for (int t = threadIdx.x; t < kHistWin; t += blockDim.x)
+        if (s_h[t]) atomicAdd(&hist[key0 + t], s_h[t]);
 }
 
 // The slab partition on the device (identical on every rank: same global
 // histogram in, same slabs out), so no host round trip sits between the
 // histogram all-reduce and the exchange.  Too few layers: slab_error + abort.
+// (Up to kPartSmem layers the histogram is staged in shared memory by the
+// whole CTA and one thread then walks it; deeper grids walk it in global
+// memory.  Launch with 4 * min(cap, kPartSmem) bytes of dynamic shared memory.)
+constexpr int kPartSmem = 12000;
 __global__ void k_slab_partition(const int* __restrict__ hist, Ctl* ctl, int G, int minLayers,
-                                 int* __restrict__ zr) {
+                                 int* __restrict__ zr, int cap) {
+    extern __shared__ int s_hist[];
     if (ctl->abort) return;
-    if (!slab_partition(hist, ctl->grid[0].dims[2], G, minLayers, zr, zr + G)) {
+    const int dz = imin_std(ctl->grid[0].dims[2], cap);  // (dims.z <= cap: k_layer_hist aborts otherwise)
+    const bool staged = dz <= kPartSmem;
+    if (staged)
+        for (int z = threadIdx.x; z < dz; z += blockDim.x) s_hist[z] = hist[z];
+    __syncthreads();
+    if (threadIdx.x != 0) return;
+    if (!slab_partition(staged ? s_hist : hist, dz, G, minLayers, zr, zr + G)) {
         ctl->slab_error = 1;
         ctl->abort = 1;
     }
@@ -80,8 +130,10 @@ __global__ void k_dest_mask(int n, const float4* __restrict__ P, const Ctl* ctl,
         for (int t = threadIdx.x; t < G * kCls; t += blockDim.x) s_cls[t] = 0;
         __syncthreads();
     }
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < n && !ctl->abort) {
+    // (grid-stride: the per-CTA counters flush from a few hundred CTAs, not
+    // one per 256 particles -- their global atomics serialise on few words)
+    const bool run = !ctl->abort;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; run && i < n; i += gridDim.x * blockDim.x) {
         const int cz = layer_of(ctl->grid[g], h, P[i].z);
         unsigned m = 0;
         for (int q = 0; q < G; ++q) {
@@ -240,30 +292,35 @@ struct alignas(64) Rec {
     int pad[3];
 };
 
-// Records [0, cnt) except the rank's own segment [skipB, skipE), which
-// never leaves the device (k_gather_self).
-__global__ void k_pack_recs(int cnt, const int* __restrict__ idx, StateSet s, Rec* __restrict__ out,
-                            int skipB = 0, int skipE = 0) {
-    const int k = blockIdx.x * blockDim.x + threadIdx.x;
-    if (k >= cnt || (k >= skipB && k < skipE)) return;
-    const int i = idx[k];
-    const float4 x = s.X[i], v = s.V[i], xs = s.XS[i];
-    Rec r;
-    r.x[0] = x.x;
-    r.x[1] = x.y;
-    r.x[2] = x.z;
-    r.v[0] = v.x;
-    r.v[1] = v.y;
-    r.v[2] = v.z;
-    r.xs[0] = xs.x;
-    r.xs[1] = xs.y;
-    r.xs[2] = xs.z;
-    r.m = xs.w;
-    r.w = s.W[i];
-    r.lam = s.L[i];
-    r.lv = s.LV[i];
-    r.pad[0] = r.pad[1] = r.pad[2] = 0;
-    out[k] = r;
+// Records for the other ranks, sized on the device (enqueued ahead of the
+// substep's host synchronisation): destination q's segment starts at
+// destStart[q] and holds destCount[q] records; the rank's own segment g is
+// skipped (k_gather_self).  Grid-stride over the records that leave.
+__global__ void k_pack_recs(const int* __restrict__ idx, StateSet s, Rec* __restrict__ out,
+                            const int* __restrict__ destCount, const int* __restrict__ destStart, int G, int g) {
+    const int total = destStart[G - 1] + destCount[G - 1];
+    const int selfB = destStart[g], selfN = destCount[g];
+    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < total - selfN; t += gridDim.x * blockDim.x) {
+        const int k = t < selfB ? t : t + selfN;
+        const int i = idx[k];
+        const float4 x = s.X[i], v = s.V[i], xs = s.XS[i];
+        Rec r;
+        r.x[0] = x.x;
+        r.x[1] = x.y;
+        r.x[2] = x.z;
+        r.v[0] = v.x;
+        r.v[1] = v.y;
+        r.v[2] = v.z;
+        r.xs[0] = xs.x;
+        r.xs[1] = xs.y;
+        r.xs[2] = xs.z;
+        r.m = xs.w;
+        r.w = s.W[i];
+        r.lam = s.L[i];
+        r.lv = s.LV[i];
+        r.pad[0] = r.pad[1] = r.pad[2] = 0;
+        out[k] = r;
+    }
 }
 
 __global__ void k_unpack_recs(int cnt, const Rec* __restrict__ in, StateSet d, int skipB = 0, int skipE = 0) {
@@ -280,10 +337,16 @@ __global__ void k_unpack_recs(int cnt, const Rec* __restrict__ in, StateSet d, i
 
 // The particles a rank keeps (its own exchange segment): straight from the
 // old state into their slots of the new local set, no record round trip.
-__global__ void k_gather_self(int m, const int* __restrict__ idx, StateSet from, StateSet to, int off) {
+// Sized on the device: destCount[g] particles at destStart[g] of idx, placed
+// after the records of ranks q < g (the exchanged class totals recvCls[q * kCls]).
+__global__ void k_gather_self(const int* __restrict__ idx, StateSet from, StateSet to,
+                              const int* __restrict__ destCount, const int* __restrict__ destStart,
+                              const int* __restrict__ recvCls, int g) {
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
-    if (k >= m) return;
-    const int i = idx[k];
+    if (k >= destCount[g]) return;
+    int off = 0;
+    for (int q = 0; q < g; ++q) off += recvCls[q * kCls];
+    const int i = idx[destStart[g] + k];
     to.X[off + k] = from.X[i];
     to.V[off + k] = from.V[i];
     to.XS[off + k] = from.XS[i];
@@ -312,77 +375,92 @@ __global__ void k_grid_reduce_unpack(Ctl* ctl, int g, const int* __restrict__ bu
     }
 }
 
-// The owned slice [b, b + m) of the sorted set back to the front of the
-// other set (this rank's state for the next substep): all six fields in one
-// launch.
-__global__ void k_copy_owned(int m, int b, StateSet from, StateSet to) {
+// K16 for the owned slice [b, b + m) of the sorted set, written to the front
+// of the other set (this rank's state for the next substep) together with
+// the fields finalize does not change: the slab path's finalize and
+// compaction in one pass.  Arithmetic and error reports as k_finalize.
+__global__ void k_finalize_owned(int m, int b, Ctl* ctl, const float4* __restrict__ Pf, StateSet from,
+                                 StateSet to, float dt, float cap, int substep) {
+    if (ctl->abort) return;
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= m) return;
-    to.X[i] = from.X[b + i];
-    to.V[i] = from.V[b + i];
-    to.XS[i] = from.XS[b + i];
-    to.W[i] = from.W[b + i];
-    to.L[i] = from.L[b + i];
-    to.LV[i] = from.LV[b + i];
-}
-
-// Contacts (findContacts().size(), sdf.hpp:226-250) and the level sum
-// (particle-iterations, solver.hpp:311-313) of the owned slots [b, e) in
-// one pass.
-__global__ void k_owned_counts(int b, int e, const float4* __restrict__ XS, const int* __restrict__ LV,
-                               const Scene* __restrict__ scene, float r, int contacts, Ctl* ctl) {
-    __shared__ int s_part[32];
-    const int i = b + blockIdx.x * blockDim.x + threadIdx.x;
-    const bool in = i < e;
-    bool c = false;
-    if (in && contacts) {
-        const float4 p = XS[i];
-        c = scene_phi(*scene, p.x, p.y, p.z) < r;
+    bool badV = false, badX = false;
+    if (i < m) {
+        const float4 s = Pf[b + i];
+        float4 v, xo;
+        finalize_particle(s, from.X[b + i], dt, cap, v, xo, badV, badX);
+        to.X[i] = xo;
+        to.V[i] = v;
+        to.XS[i] = s;
+        to.W[i] = from.W[b + i];
+        to.L[i] = from.L[b + i];
+        to.LV[i] = from.LV[b + i];
     }
-    int v = warp_sum_i(in ? LV[i] : 0);
-    if ((threadIdx.x & 31) == 0) s_part[threadIdx.x >> 5] = v;
-    __syncthreads();
-    if (threadIdx.x < 32) {  // one atomic per block
-        v = threadIdx.x < (blockDim.x >> 5) ? s_part[threadIdx.x] : 0;
-        v = warp_sum_i(v);
-        if (threadIdx.x == 0 && v) atomicAdd(&ctl->total_iterations, (unsigned long long)v);
-    }
-    if (contacts) block_count_add(&ctl->contacts, c);
+    finalize_report(ctl, badV, badX, i, substep);
 }
 
 // The iteration order's levels (0, never active, outside [b, e) or inside
 // the excluded [xb, xe)) and their per-tile histogram, in one pass.
-__global__ void __launch_bounds__(kTileThreads) k_mask_level_tiles(int n, const Ctl* ctl,
+// With ob < oe also the level sum of the owned slots [ob, oe) (the rank's
+// particle-iterations, solver.hpp:311-313) into ctl->total_iterations.
+__global__ void __launch_bounds__(kTileThreads) k_mask_level_tiles(int n, Ctl* ctl,
                                                                    const int* __restrict__ LV, int b, int e,
                                                                    int xb, int xe, int* __restrict__ LVo,
                                                                    int nMax, int numTiles,
-                                                                   int* __restrict__ tileCount) {
+                                                                   int* __restrict__ tileCount, int ob = 0,
+                                                                   int oe = 0) {
     if (ctl->abort) return;
     extern __shared__ int s_cnt[];
+    __shared__ int s_tot;
     for (int l = threadIdx.x; l <= nMax; l += blockDim.x) s_cnt[l] = 0;
+    if (threadIdx.x == 0) s_tot = 0;
     __syncthreads();
+    int tot = 0;
     for (int r = 0; r < kTileRounds; ++r) {
         const int k = blockIdx.x * kTileSize + r * kTileThreads + threadIdx.x;
         if (k < n) {
-            const int lv = (k >= b && k < e && !(k >= xb && k < xe)) ? LV[k] : 0;
+            const int raw = LV[k];
+            const int lv = (k >= b && k < e && !(k >= xb && k < xe)) ? raw : 0;
             LVo[k] = lv;
             atomicAdd(&s_cnt[imin_std(imax_std(lv, 0), nMax)], 1);
+            if (k >= ob && k < oe) tot += raw;
         }
     }
+    tot = warp_sum_i(tot);
+    if ((threadIdx.x & 31) == 0 && tot) atomicAdd(&s_tot, tot);
     __syncthreads();
     for (int l = threadIdx.x; l <= nMax; l += blockDim.x)
         tileCount[(long long)l * numTiles + blockIdx.x] = s_cnt[l];
+    if (threadIdx.x == 0 && s_tot) atomicAdd(&ctl->total_iterations, (unsigned long long)s_tot);
 }
 
 // Metrics ghost records: (x, y, z, mass) + owned flag in the w of a second
 // float? -- packed as float4 xyzm and an int flag array.
-__global__ void k_pack_pm(int cnt, const int* __restrict__ idx, const float4* __restrict__ X,
-                          const float4* __restrict__ XS, float4* __restrict__ out) {
-    const int k = blockIdx.x * blockDim.x + threadIdx.x;
-    if (k >= cnt) return;
-    const int i = idx[k];
-    const float4 x = X[i];
-    out[k] = make_float4(x.x, x.y, x.z, XS[i].w);
+// Sized on the device (ahead of the host synchronisation, as k_pack_recs):
+// every destination's (x, y, z, mass) records; the rank's own segment goes
+// straight to its place in the received array (after the records of ranks
+// q < g) together with its owned flag, the others' flags are cleared.
+__global__ void k_pack_pm(const int* __restrict__ idx, const float4* __restrict__ X,
+                          const float4* __restrict__ XS, float4* __restrict__ out,
+                          const int* __restrict__ destCount, const int* __restrict__ destStart,
+                          const int* __restrict__ recvCls, int G, int g, float4* __restrict__ recv,
+                          int* __restrict__ ownedFlag) {
+    const int total = destStart[G - 1] + destCount[G - 1];
+    const int selfB = destStart[g], selfE = selfB + destCount[g];
+    int off = 0, nRecv = 0;
+    for (int q = 0; q < G; ++q) {
+        if (q < g) off += recvCls[q * kCls];
+        nRecv += recvCls[q * kCls];
+    }
+    const int stride = gridDim.x * blockDim.x;
+    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < total; k += stride) {
+        const int i = idx[k];
+        const float4 x = X[i];
+        const float4 r = make_float4(x.x, x.y, x.z, XS[i].w);
+        if (k >= selfB && k < selfE) recv[off + k - selfB] = r;
+        else out[k] = r;
+    }
+    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < nRecv; k += stride)
+        ownedFlag[k] = (k >= off && k < off + selfE - selfB) ? 1 : 0;
 }
 
 // Densities of the owned particles of a sorted (position, mass) array whose

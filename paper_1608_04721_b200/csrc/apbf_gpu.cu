@@ -201,13 +201,16 @@ struct Workspace {
 
     // UniformGrid::build on float4 positions P (AABB already in grid g):
     // params, histogram, scan, stable counting sort -> perm, cellStart.
-    void run_grid(int g, const float4* P, int n, float h, float pad, bool contacts, float radius) {
+    // ownLo/ownHi (slab mode, device pointers): contacts of the owned layers
+    // only; params = false when the caller already ran k_grid_params for g.
+    void run_grid(int g, const float4* P, int n, float h, float pad, bool contacts, float radius,
+                  const int* ownLo = nullptr, const int* ownHi = nullptr, bool params = true) {
         ensure_cells();
         ensure_particles(n);
-        KL(k_grid_params<<<1, 1, 0, stream>>>(ctl.p, g, h, pad));
+        if (params) KL(k_grid_params<<<1, 1, 0, stream>>>(ctl.p, g, h, pad));
         KL(k_zero_cells<<<4 * 148, 256, 0, stream>>>(ctl.p, g, cellCount.p));
         KL(k_cell_keys<<<blocks(n, 256), 256, 0, stream>>>(n, P, ctl.p, g, h, cellCount.p, key.p, slot.p,
-                                                        scene.p, radius, contacts ? 1 : 0));
+                                                        scene.p, radius, contacts ? 1 : 0, ownLo, ownHi));
         KL(k_scan_reduce<<<kScanGrid, kScanBlock, 0, stream>>>(ctl.p, g, cellCount.p, partial.p));
         KL(k_scan_partials<<<1, kScanBlock, 0, stream>>>(ctl.p, partial.p, kScanGrid));
         KL(k_scan_apply<<<kScanGrid, kScanBlock, 0, stream>>>(ctl.p, g, cellCount.p, partial.p));
@@ -501,6 +504,8 @@ struct apbf_gpu_solver {
         if (ev_lod_join) cudaEventDestroy(ev_lod_join);
         if (ev_halo_ready) cudaEventDestroy(ev_halo_ready);
         if (ev_halo_done) cudaEventDestroy(ev_halo_done);
+        if (ev_cls) cudaEventDestroy(ev_cls);
+        if (hostCls) cudaFreeHost(hostCls);
     }
 
     void allocate(int nn) {
@@ -1529,13 +1534,20 @@ struct apbf_gpu_solver {
     int* clsSend = nullptr;
     int* clsRecv = nullptr;
     DBuf<int> gridRed;           // [~abort, lo(3), ~hi(3)]: the grid's one MIN all-reduce
-    std::vector<int> hostCls;    // [send G*kCls | recv G*kCls | ctl flags]
+    int* hostCls = nullptr;      // pinned [send G*kCls | recv G*kCls] (an async read: the
+                                 // host keeps enqueueing while it lands)
 
     // The per-destination totals and classes of an exchange: sent on the
     // stream ahead of the records (kCls ints per peer), then ONE host
     // synchronisation reads what this rank sends and receives together with
     // the (already all-reduced) abort flags.  Returns false on abort.
-    bool exchange_classes(Transport& T, int ncls) {
+    // Split in two: exchange_classes_begin enqueues the exchange and the
+    // reads and records ev_cls; the caller then enqueues the device-sized
+    // work that does not need the host (the destination expansion, the
+    // record pack, the self gather) so that the GPU keeps running while the
+    // host waits in exchange_classes_end.
+    cudaEvent_t ev_cls = nullptr;
+    void exchange_classes_begin(Transport& T, int ncls) {
         const int G = T.size(), g = T.rank();
         cudaStream_t st = ws.stream;
         std::vector<const void*> sp(G);
@@ -1549,11 +1561,27 @@ struct apbf_gpu_solver {
         CK(cudaMemcpyAsync(clsRecv + (size_t)g * kCls, clsSend + (size_t)g * kCls, sizeof(int) * ncls,
                            cudaMemcpyDeviceToDevice, st));
         T.alltoallv(sp.data(), sb.data(), rp.data(), rb.data(), st);
-        hostCls.resize((size_t)2 * G * kCls);
-        CK(cudaMemcpyAsync(hostCls.data(), clsSend, sizeof(int) * 2 * G * kCls, cudaMemcpyDeviceToHost, st));
+        if (!hostCls) CK(cudaMallocHost(&hostCls, sizeof(int) * 2 * kMaxRanks * kCls));
+        CK(cudaMemcpyAsync(hostCls, clsSend, sizeof(int) * 2 * G * kCls, cudaMemcpyDeviceToHost, st));
         CK(cudaMemcpyAsync(ws.h_ctl, ws.ctl.p, sizeof(Ctl), cudaMemcpyDeviceToHost, st));
-        CK(cudaStreamSynchronize(st));
+        if (!ev_cls) CK(cudaEventCreateWithFlags(&ev_cls, cudaEventDisableTiming));
+        CK(cudaEventRecord(ev_cls, st));
+    }
+    bool exchange_classes_end() {
+        CK(cudaEventSynchronize(ev_cls));
         return !ws.h_ctl->abort;
+    }
+    // The stable expansion of destMask[0, n) by destination into sendIdx,
+    // per-destination counts and starts on the device.
+    void expand_dest(int G) {
+        cudaStream_t st = ws.stream;
+        const int tiles = std::max(1, (n + kTileSize - 1) / kTileSize);
+        destTile.ensure((size_t)G * tiles);
+        KL(k_mask_tile_counts<<<tiles, kTileThreads, 0, st>>>(n, destMask.p, G, tiles, destTile.p));
+        KL(k_mask_scan<<<G, 1024, 0, st>>>(tiles, destTile.p, destCountD.p));
+        KL(k_dest_starts<<<1, 32, 0, st>>>(destCountD.p, G, destStartD.p));
+        KL(k_mask_scatter<<<tiles, kTileThreads, 0, st>>>(n, destMask.p, G, tiles, destTile.p, destStartD.p,
+                                                        sendIdx.p));
     }
 
     // One slab frame.  Per substep the host synchronises ONCE (after the
@@ -1608,20 +1636,31 @@ struct apbf_gpu_solver {
             // slabs: equal-work split (sum of 1 + level per layer) of the
             // global histogram, computed on the device
             CK(cudaMemsetAsync(layerHist.p, 0, sizeof(int) * layer_cap, st));
-            KL(k_layer_hist<<<blocks(n, 256), 256, 0, st>>>(n, src.XS, src.LV, ctl, 0, cfg.h, layerHist.p,
+            KL(k_layer_hist<<<std::max(1, std::min(blocks(n, 256 * kHistItems), 148 * 8)), 256, 0, st>>>(n, src.XS, src.LV, ctl, 0, cfg.h, layerHist.p,
                                                           layer_cap));
             T.allreduce(layerHist.p, layer_cap, RType::I32, ROp::Sum, st);
-            KL(k_slab_partition<<<1, 1, 0, st>>>(layerHist.p, ctl, G, 2, zRange.p));
+            KL(k_slab_partition<<<1, 256, sizeof(int) * std::min(layer_cap, kPartSmem), st>>>(
+                layerHist.p, ctl, G, 2, zRange.p, layer_cap));
             // migration + halo in one all-to-all, previous global order kept
             CK(cudaMemsetAsync(clsSend, 0, sizeof(int) * G * kCls, st));
-            KL(k_dest_mask<<<blocks(n, 256), 256, 0, st>>>(n, src.XS, ctl, 0, cfg.h, zRange.p, zRange.p + G,
+            KL(k_dest_mask<<<std::max(1, std::min(blocks(n, 256), 148 * 4)), 256, 0, st>>>(n, src.XS, ctl, 0, cfg.h, zRange.p, zRange.p + G,
                                                          G, 2, destMask.p, clsSend));
             tmark("pre-exchange");
-            if (!exchange_classes(T, kCls)) break;  // the substep's one host synchronisation
+            exchange_classes_begin(T, kCls);
+            // device-sized, ahead of the host synchronisation: expansion by
+            // destination, records for the other ranks, and this rank's own
+            // segment straight from the old state into the new local set
+            expand_dest(G);
+            if (G > 1)
+                KL(k_pack_recs<<<std::min(blocks(n, 256), 148 * 8), 256, 0, st>>>(sendIdx.p, src, sendRec.p,
+                                                                                 destCountD.p, destStartD.p, G, g));
+            KL(k_gather_self<<<blocks(n, 256), 256, 0, st>>>(sendIdx.p, src, dst, destCountD.p, destStartD.p,
+                                                            clsRecv, g));
+            if (!exchange_classes_end()) break;  // the substep's one host synchronisation
             tmark("class sync");
             // sizes: what goes where, and this rank's layout after the sort
-            const int* sendC = hostCls.data();
-            const int* recvC = hostCls.data() + (size_t)G * kCls;
+            const int* sendC = hostCls;
+            const int* recvC = hostCls + (size_t)G * kCls;
             std::vector<long long> sendCnt(G), sendStart(G), recvCnt(G), roff(G);
             long long nsend = 0, nLocal = 0;
             long long lowG0 = 0, lowG1 = 0, own2lo = 0, hiG0 = 0, hiG1 = 0, ownHi2 = 0;
@@ -1647,19 +1686,6 @@ struct apbf_gpu_solver {
             const int ownB = (int)(lowG0 + lowG1), l1B = (int)lowG0;
             const int ownE = (int)(nLocal - hiG0 - hiG1), l1E = (int)(nLocal - hiG1);
             const int lowEnd = (int)(ownB + own2lo), highB = (int)(ownE - ownHi2);
-            const int tiles = std::max(1, (n + kTileSize - 1) / kTileSize);
-            destTile.ensure((size_t)G * tiles);
-            KL(k_mask_tile_counts<<<tiles, kTileThreads, 0, st>>>(n, destMask.p, G, tiles, destTile.p));
-            KL(k_mask_scan<<<G, 1024, 0, st>>>(tiles, destTile.p, destCountD.p));
-            KL(k_dest_starts<<<1, 32, 0, st>>>(destCountD.p, G, destStartD.p));
-            KL(k_mask_scatter<<<tiles, kTileThreads, 0, st>>>(n, destMask.p, G, tiles, destTile.p, destStartD.p,
-                                                            sendIdx.p));
-            // records only for the other ranks; this rank's own segment goes
-            // straight from the old state (src) into the new local set (dst)
-            const int selfB = (int)sendStart[g], selfE = (int)(sendStart[g] + sendCnt[g]);
-            if (nsend > sendCnt[g])
-                KL(k_pack_recs<<<blocks(nsend, 256), 256, 0, st>>>((int)nsend, sendIdx.p, src, sendRec.p, selfB,
-                                                                 selfE));
             std::vector<const void*> sp(G);
             std::vector<void*> rp(G);
             std::vector<size_t> sb(G), rb(G);
@@ -1671,9 +1697,6 @@ struct apbf_gpu_solver {
             }
             T.alltoallv(sp.data(), sb.data(), rp.data(), rb.data(), st);
             const int nL = (int)nLocal;
-            if (sendCnt[g])
-                KL(k_gather_self<<<blocks(sendCnt[g], 256), 256, 0, st>>>((int)sendCnt[g], sendIdx.p + selfB, src,
-                                                                        dst, (int)roff[g]));
             if (nL > sendCnt[g])
                 KL(k_unpack_recs<<<blocks(nL, 256), 256, 0, st>>>(nL, recvRec.p, dst, (int)roff[g],
                                                                 (int)(roff[g] + sendCnt[g])));
@@ -1682,15 +1705,14 @@ struct apbf_gpu_solver {
             std::swap(src, dst);
             tmark("exchange");
             // local stable sort by global cell == global order restricted
-            ws.run_grid(0, src.XS, nL, cfg.h, cfg.h, false, radius);
+            // (contacts of the owned layers counted on the way; grid params
+            // already set for this grid above)
+            ws.run_grid(0, src.XS, nL, cfg.h, cfg.h, scene.n > 0, radius, zRange.p + g, zRange.p + G + g, false);
             const int tilesL = std::max(1, (nL + kTileSize - 1) / kTileSize);
             const int smemG = (nMax + 1) * (int)sizeof(int);
             KL(k_gather<<<tilesL, kTileThreads, smemG, st>>>(nL, ctl, ws.perm.p, src, dst, nMax, tilesL,
                                                            tileCount.p));
             const int nOwn = ownE - ownB;
-            if (nOwn > 0)
-                KL(k_owned_counts<<<blocks(nOwn, 256), 256, 0, st>>>(ownB, ownE, dst.XS, dst.LV, ws.scene.p, radius,
-                                                                   scene.n > 0 ? 1 : 0, ctl));
             // iteration order over owned + layer-1 ghosts (lambda is computed
             // redundantly for the latter), outer ghosts never active.  With
             // neighbours the particles split into two iteration sets: A, the
@@ -1703,9 +1725,11 @@ struct apbf_gpu_solver {
             // lists and sums: bitwise the single-set results.)
             const int a0 = g > 0 ? lowEnd : ownB, a1 = g < G - 1 ? highB : ownE;
             const bool split = G > 1 && !cfg.record_residuals && a0 < a1;
-            auto bucket = [&](int b, int e, int xb, int xe) {
+            // (the first bucket also sums the owned levels: the rank's particle-iterations)
+            auto bucket = [&](int b, int e, int xb, int xe, bool total) {
                 KL(k_mask_level_tiles<<<tilesL, kTileThreads, smemG, st>>>(nL, ctl, dst.LV, b, e, xb, xe, LVo.p,
-                                                                          nMax, tilesL, tileCount.p));
+                                                                          nMax, tilesL, tileCount.p,
+                                                                          total ? ownB : 0, total ? ownE : 0));
                 KL(k_level_scan<<<nMax + 1, 1024, 0, st>>>(ctl, tilesL, tileCount.p, levelCount.p));
                 KL(k_level_finish<<<1, 32, 0, st>>>(ctl, nL, nMax, levelCount.p, activeCount.p, bucketStart.p, 0));
                 KL(k_level_scatter<<<tilesL, kTileThreads, 9 * smemG, st>>>(nL, ctl, LVo.p, nMax, tilesL,
@@ -1714,12 +1738,12 @@ struct apbf_gpu_solver {
             };
             if (split) {
                 ensure_set_b();
-                bucket(a0, a1, 0, 0);  // set A
+                bucket(a0, a1, 0, 0, true);  // set A
                 swap_sets();
-                bucket(l1B, l1E, a0, a1);  // set B
+                bucket(l1B, l1E, a0, a1, false);  // set B
                 swap_sets();
             } else {
-                bucket(l1B, l1E, 0, 0);
+                bucket(l1B, l1E, 0, 0, true);
             }
             // pre-stabilization of every local copy with level < S (owners and
             // ghost copies compute the same values); errors from owned only
@@ -1785,12 +1809,11 @@ struct apbf_gpu_solver {
             ownB_ = 0;
             ownE_ = 0x7fffffff;
             float4* Pf = P[nMax & 1];
+            // finalize the owned particles into the front of the other set:
+            // in order, this rank's state for the next substep
             if (nOwn > 0)
-                KL(k_finalize<<<blocks(nOwn, 256), 256, 0, st>>>(nOwn, ctl, Pf + ownB, dst.XS + ownB, dst.X + ownB,
-                                                               dst.V + ownB, dt, cap, Pf != dst.XS ? 1 : 0, s));
+                KL(k_finalize_owned<<<blocks(nOwn, 256), 256, 0, st>>>(nOwn, ownB, ctl, Pf, dst, src, dt, cap, s));
             LAUNCH_CHECK();
-            // keep only the owned particles, in order, as this rank's state
-            if (nOwn > 0) KL(k_copy_owned<<<blocks(nOwn, 256), 256, 0, st>>>(nOwn, ownB, dst, src));
             n = nOwn;
             localPost[s] = n;
             cur ^= 1;  // the owned state now lives in the other set (src after the swap)
@@ -1832,11 +1855,16 @@ struct apbf_gpu_solver {
         T.allreduce(spanHi.p, G, RType::I32, ROp::Max, st);
         KL(k_metrics_ranges<<<1, 32, 0, st>>>(G, g, spanLo.p, spanHi.p));
         CK(cudaMemsetAsync(clsSend, 0, sizeof(int) * G * kCls, st));
-        KL(k_dest_mask<<<blocks(n, 256), 256, 0, st>>>(n, cs.X, ctl, 1, cfg.h, spanLo.p, spanHi.p, G, 1,
+        KL(k_dest_mask<<<std::max(1, std::min(blocks(n, 256), 148 * 4)), 256, 0, st>>>(n, cs.X, ctl, 1, cfg.h, spanLo.p, spanHi.p, G, 1,
                                                      destMask.p, clsSend));
-        if (!exchange_classes(T, 1)) return;
-        const int* sendC = hostCls.data();
-        const int* recvC = hostCls.data() + (size_t)G * kCls;
+        exchange_classes_begin(T, 1);
+        expand_dest(G);
+        KL(k_pack_pm<<<std::min(blocks(n, 256), 148 * 8), 256, 0, st>>>(sendIdx.p, cs.X, cs.XS, sendPM.p,
+                                                                       destCountD.p, destStartD.p, clsRecv, G, g,
+                                                                       recvPM.p, ownedFlag.p));
+        if (!exchange_classes_end()) return;
+        const int* sendC = hostCls;
+        const int* recvC = hostCls + (size_t)G * kCls;
         std::vector<long long> sendCnt(G), sendStart(G), recvCnt(G), roff(G);
         long long nsend = 0, nM = 0;
         for (int q = 0; q < G; ++q) {
@@ -1849,15 +1877,6 @@ struct apbf_gpu_solver {
         }
         if (nM > n_capacity || nsend > send_capacity)  // cannot happen: see set_state_local
             fail(APBF_ERR_RUNTIME, "internal: slab metrics exchange larger than its worst-case capacity");
-        const int tiles = std::max(1, (n + kTileSize - 1) / kTileSize);
-        destTile.ensure((size_t)G * tiles);
-        KL(k_mask_tile_counts<<<tiles, kTileThreads, 0, st>>>(n, destMask.p, G, tiles, destTile.p));
-        KL(k_mask_scan<<<G, 1024, 0, st>>>(tiles, destTile.p, destCountD.p));
-        KL(k_dest_starts<<<1, 32, 0, st>>>(destCountD.p, G, destStartD.p));
-        KL(k_mask_scatter<<<tiles, kTileThreads, 0, st>>>(n, destMask.p, G, tiles, destTile.p, destStartD.p,
-                                                        sendIdx.p));
-        if (nsend > 0)
-            KL(k_pack_pm<<<blocks(nsend, 256), 256, 0, st>>>((int)nsend, sendIdx.p, cs.X, cs.XS, sendPM.p));
         std::vector<const void*> sp(G);
         std::vector<void*> rp(G);
         std::vector<size_t> sb(G), rb(G);
@@ -1867,16 +1886,9 @@ struct apbf_gpu_solver {
             rp[q] = recvPM.p + roff[q];
             rb[q] = sizeof(float4) * recvCnt[q];
         }
-        if (sendCnt[g])
-            CK(cudaMemcpyAsync(recvPM.p + roff[g], sendPM.p + sendStart[g], sizeof(float4) * sendCnt[g],
-                               cudaMemcpyDeviceToDevice, st));
         T.alltoallv(sp.data(), sb.data(), rp.data(), rb.data(), st);
         const int nm = (int)nM;
-        CK(cudaMemsetAsync(ownedFlag.p, 0, sizeof(int) * std::max(nm, 1), st));
-        if (sendCnt[g]) {
-            KL(k_fill_int<<<blocks(sendCnt[g], 256), 256, 0, st>>>(ownedFlag.p + roff[g], (int)sendCnt[g], 1));
-        }
-        ws.run_grid(1, recvPM.p, nm, cfg.h, cfg.h, false, radius);
+        ws.run_grid(1, recvPM.p, nm, cfg.h, cfg.h, false, radius, nullptr, nullptr, false);
         KL(k_gather_posmass<<<blocks(nm, 256), 256, 0, st>>>(nm, ctl, ws.perm.p, recvPM.p, recvPM.p, sortedPM.p));
         KL(k_gather_int<<<blocks(nm, 256), 256, 0, st>>>(nm, ws.perm.p, ownedFlag.p, ownedSorted.p));
         KL(k_density_stats_owned<<<blocks(nm, 256), 256, 0, st>>>(nm, ctl, sortedPM.p, ownedSorted.p,
