@@ -768,7 +768,7 @@ struct apbf_gpu_solver {
         const int why = ws.h_ctl->list_overflow;
         if ((why & 1) && packed_lists) nbrCap = std::max<long long>(nbrCap * 2, (long long)(used * 3 / 2));
         if ((why & 1) && !packed_lists) {
-            const int want = std::max(list_stride + 16, (int)used_fb + 8);
+            const int want = list_rows(std::max(list_stride + 16, (int)used_fb + 8));
             if (want > kMaxListStride) {
                 // a few very long lists: a uniform stride would cost n x max;
                 // switch to per-warp slabs from the allocating builder
@@ -2411,8 +2411,8 @@ int32_t apbf_gpu_neighbor_lists(int32_t n, const float* positions, float h, floa
             if (indices_capacity < total) fail(APBF_ERR_INVALID_ARGUMENT, "indices capacity too small");
             long long w = 0;
             for (int i = 0; i < n; ++i) {
-                const long long b0 = hb[i >> 5] + (i & 31);
-                for (int e = 0; e < hc[i]; ++e) indices[w++] = hl[b0 + (long long)e * 32];
+                const long long b0 = hb[i >> 5] + 4 * (i & 31);  // chunked slab layout (list_at)
+                for (int e = 0; e < hc[i]; ++e) indices[w++] = hl[b0 + ((long long)(e >> 2) << 7) + (e & 3)];
             }
         }
     });

@@ -37,10 +37,10 @@ __global__ void k_post_omega(int n, const Ctl* ctl, const int* __restrict__ orde
     const int i = order[k];
     const float4 xi = X[i], vi = V[i];
     const int cnt = nbrCount[k];
-    const int* lst = nbr + groupBase[k >> 5] + (k & 31);
+    const int* lst = list_lane(nbr, groupBase[k >> 5], k & 31);
     float ox = 0.f, oy = 0.f, oz = 0.f, sx = 0.f, sy = 0.f, sz = 0.f;
     for (int e = 0; e < cnt; ++e) {
-        const int j = lst[e * 32];
+        const int j = list_at(lst, e);
         if (j == i) continue;
         const float4 xj = X[j], vj = V[j];
         const float rx = xi.x - xj.x, ry = xi.y - xj.y, rz = xi.z - xj.z;
@@ -74,11 +74,11 @@ __global__ void k_post_apply(int n, Ctl* ctl, const int* __restrict__ order, con
     const int i = order[k];
     const float4 xi = X[i], oi = Om[i];
     const int cnt = nbrCount[k];
-    const int* lst = nbr + groupBase[k >> 5] + (k & 31);
+    const int* lst = list_lane(nbr, groupBase[k >> 5], k & 31);
     float ex = 0.f, ey = 0.f, ez = 0.f;
     if (eps != 0.0f) {
         for (int e = 0; e < cnt; ++e) {
-            const int j = lst[e * 32];
+            const int j = list_at(lst, e);
             if (j == i) continue;
             const float4 xj = X[j];
             const float rx = xi.x - xj.x, ry = xi.y - xj.y, rz = xi.z - xj.z;
