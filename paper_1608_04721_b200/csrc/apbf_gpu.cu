@@ -111,6 +111,10 @@ inline int blocks(long long n, int t) { return (int)std::max<long long>(1, (n + 
 // Bumped by every device (re)allocation: a captured frame graph holds raw
 // pointers, so it is re-recorded only when this changes.
 static unsigned long long g_alloc_gen = 0;
+// Set while a slab-frame segment is being recorded into a CUDA graph: a
+// device allocation there would synchronise the capturing thread (the slab
+// path preallocates every buffer its segments use, set_state_local).
+static thread_local bool g_segment_capture = false;
 
 template <class T>
 struct DBuf {
@@ -127,6 +131,8 @@ struct DBuf {
     }
     void ensure(size_t m) {
         if (m <= n && p) return;
+        if (g_segment_capture)
+            throw ApiError{APBF_ERR_RUNTIME, "", -1, "internal: device allocation during slab graph capture"};
         release();
         const size_t bytes = sizeof(T) * std::max<size_t>(m, 1) + kBufSlack;
         CK(cudaMalloc(&p, bytes));
@@ -1406,6 +1412,20 @@ struct apbf_gpu_solver {
         destCountD.ensure(kMaxRanks);
         destStartD.ensure(kMaxRanks);
         minmax.ensure(2);
+        // every buffer the slab segments use, at its worst case: a recorded
+        // segment must not allocate (g_segment_capture)
+        const long long tilesMax = (n_capacity + kTileSize - 1) / kTileSize;
+        destTile.ensure((size_t)std::max(G, 1) * (size_t)std::max<long long>(tilesMax, 1));
+        ws.ensure_cells();
+        ws.ensure_particles((size_t)n_capacity);
+        if (G > 1) ensure_set_b();
+        layerHist.ensure(layer_cap);
+        gridRed.ensure(8);
+        clsBuf.ensure((size_t)2 * kMaxRanks * kCls);
+        spanLo.ensure(kMaxRanks);
+        spanHi.ensure(kMaxRanks);
+        if (!hostCls) CK(cudaMallocHost(&hostCls, sizeof(int) * 2 * kMaxRanks * kCls));
+        if (!ev_cls) CK(cudaEventCreateWithFlags(&ev_cls, cudaEventDisableTiming));
         cur = 0;
         upload_state(nloc, x, xs, v, mass, inv_mass, lambda, level);
     }
@@ -1462,12 +1482,15 @@ struct apbf_gpu_solver {
         ws.dist.ensure(std::max(nn, 1));
         ws.keys.ensure(std::max(nn, 1));
         const bool dtvs = lod.model == APBF_LOD_DTVS;
+        const size_t px = (size_t)cam.width * cam.height;
         if (dtvs) {
-            const CamFrame f = make_frame(cam);
-            const size_t px = (size_t)cam.width * cam.height;
             ws.depth.ensure(px);
             ws.rays.ensure(px);
             ws.raysa.ensure(px);
+        }
+        seg_begin();  // (buffers sized above: the recording allocates nothing)
+        if (dtvs) {
+            const CamFrame f = make_frame(cam);
             KL(k_splat_prep<<<blocks((long long)px, 256), 256, 0, st>>>(f, ws.depth.p, ws.rays.p, ws.raysa.p));
             KL(k_splat<<<blocks(nn, 256), 256, 0, st>>>(nn, X, radius, f, ws.depth.p, ws.rays.p, ws.raysa.p));
             T.allreduce(ws.depth.p, px, RType::I32, ROp::Min, st);  // positive float bits: int order
@@ -1491,6 +1514,7 @@ struct apbf_gpu_solver {
         KL(k_lod_map<<<blocks(nn, 256), 256, 0, st>>>(nn, ws.ctl.p, ws.dist.p, ws.keys.p, dtvs ? 1 : 0,
                                                      lod.n_min, lod.n_max, LV));
         LAUNCH_CHECK();
+        seg_end(segLod);
     }
 
     cudaStream_t comm_stream = nullptr;  // slab mode: the x* halo exchange (overlapped)
@@ -1508,7 +1532,7 @@ struct apbf_gpu_solver {
     std::vector<TracePt> trace_;
     bool slab_trace = std::getenv("APBF_SLAB_TRACE") != nullptr;
     void tmark(const char* what) {
-        if (!slab_trace) return;
+        if (!slab_trace || capturing) return;
         TracePt t{what, std::chrono::steady_clock::now(), nullptr};
         CK(cudaEventCreate(&t.ev));
         CK(cudaEventRecord(t.ev, ws.stream));
@@ -1541,6 +1565,66 @@ struct apbf_gpu_solver {
     // stream ahead of the records (kCls ints per peer), then ONE host
     // synchronisation reads what this rank sends and receives together with
     // the (already all-reduced) abort flags.  Returns false on abort.
+    // Slab-frame segments recorded into CUDA graphs (transports whose
+    // collectives only enqueue stream work: NCCL).  Each substep re-records
+    // its segment with that substep's sizes and updates the instantiated
+    // graph in place (cudaGraphExecUpdate; a fresh instantiate when the
+    // topology changed), then launches it: one launch instead of ~20 short
+    // eager ones.  The loopback transport synchronises on the host inside its
+    // collectives, so it runs the same code eagerly.  APBF_SLAB_GRAPHS=0 (or
+    // APBF_GRAPHS=0, or APBF_SLAB_TRACE) records nothing.
+    struct SegGraph {
+        cudaGraphExec_t exec = nullptr;
+        SegGraph() = default;
+        SegGraph(const SegGraph&) = delete;
+        SegGraph& operator=(const SegGraph&) = delete;
+        ~SegGraph() {
+            if (exec) cudaGraphExecDestroy(exec);
+        }
+    };
+    SegGraph segLod, segPre, segPost, segIter, segMetPre, segMetPost;
+    bool seg_on = false;
+    bool slab_graphs = [] {
+        const char* e = std::getenv("APBF_SLAB_GRAPHS");
+        return !(e && e[0] == '0');
+    }();
+    void seg_begin() {
+        if (!seg_on) return;
+        CK(cudaStreamBeginCapture(ws.stream, cudaStreamCaptureModeThreadLocal));
+        capturing = true;
+        g_segment_capture = true;
+    }
+    void seg_end(SegGraph& sg) {
+        if (!seg_on) return;
+        capturing = false;
+        g_segment_capture = false;
+        cudaGraph_t g = nullptr;
+        CK(cudaStreamEndCapture(ws.stream, &g));
+        if (sg.exec) {
+            cudaGraphExecUpdateResultInfo info;
+            if (cudaGraphExecUpdate(sg.exec, g, &info) != cudaSuccess) {
+                (void)cudaGetLastError();
+                cudaGraphExecDestroy(sg.exec);
+                sg.exec = nullptr;
+            }
+        }
+        cudaError_t e = cudaSuccess;
+        if (!sg.exec) e = cudaGraphInstantiate(&sg.exec, g, 0);
+        cudaGraphDestroy(g);
+        CK(e);
+        CK(cudaGraphLaunch(sg.exec, ws.stream));
+    }
+    // An exception while recording: leave capture mode, drop the recording.
+    void seg_cancel() {
+        if (!g_segment_capture) return;
+        capturing = false;
+        g_segment_capture = false;
+        cudaGraph_t g = nullptr;
+        cudaStreamEndCapture(ws.stream, &g);
+        if (g) cudaGraphDestroy(g);
+        (void)cudaGetLastError();
+    }
+
     // Split in two: exchange_classes_begin enqueues the exchange and the
     // reads and records ev_cls; the caller then enqueues the device-sized
     // work that does not need the host (the destination expansion, the
@@ -1561,11 +1645,9 @@ struct apbf_gpu_solver {
         CK(cudaMemcpyAsync(clsRecv + (size_t)g * kCls, clsSend + (size_t)g * kCls, sizeof(int) * ncls,
                            cudaMemcpyDeviceToDevice, st));
         T.alltoallv(sp.data(), sb.data(), rp.data(), rb.data(), st);
-        if (!hostCls) CK(cudaMallocHost(&hostCls, sizeof(int) * 2 * kMaxRanks * kCls));
         CK(cudaMemcpyAsync(hostCls, clsSend, sizeof(int) * 2 * G * kCls, cudaMemcpyDeviceToHost, st));
         CK(cudaMemcpyAsync(ws.h_ctl, ws.ctl.p, sizeof(Ctl), cudaMemcpyDeviceToHost, st));
-        if (!ev_cls) CK(cudaEventCreateWithFlags(&ev_cls, cudaEventDisableTiming));
-        CK(cudaEventRecord(ev_cls, st));
+        rec(ev_cls);  // (an external event node while a segment is recorded)
     }
     bool exchange_classes_end() {
         CK(cudaEventSynchronize(ev_cls));
@@ -1594,6 +1676,16 @@ struct apbf_gpu_solver {
     // sequence at the same point.
     void run_frame_dist(Transport& T, long long nAll, bool assign_lod, const apbf_camera* cam,
                         const apbf_lod_config* lod) {
+        seg_on = use_graphs && slab_graphs && T.capturable() && !slab_trace;
+        try {
+            run_frame_dist_body(T, nAll, assign_lod, cam, lod);
+        } catch (...) {
+            seg_cancel();
+            throw;
+        }
+    }
+    void run_frame_dist_body(Transport& T, long long nAll, bool assign_lod, const apbf_camera* cam,
+                             const apbf_lod_config* lod) {
         const int G = T.size(), g = T.rank();
         cudaStream_t st = ws.stream;
         Ctl* ctl = ws.ctl.p;
@@ -1624,6 +1716,7 @@ struct apbf_gpu_solver {
             NvtxRange range("apbf slab substep");
             localPre[s] = n;
             StateSet src = set[cur].view(), dst = set[cur ^ 1].view();
+            seg_begin();  // segment 1: everything up to the host synchronisation
             KL(k_substep_reset<<<1, 1, 0, st>>>(ctl));
             KL(k_predict<<<blocks(n, kAabbBlock), kAabbBlock, 0, st>>>(n, src.X, src.V, src.V, src.XS, src.XS, dt,
                                                       cfg.gravity[0], cfg.gravity[1], cfg.gravity[2], ctl, s));
@@ -1656,6 +1749,7 @@ struct apbf_gpu_solver {
                                                                                  destCountD.p, destStartD.p, G, g));
             KL(k_gather_self<<<blocks(n, 256), 256, 0, st>>>(sendIdx.p, src, dst, destCountD.p, destStartD.p,
                                                             clsRecv, g));
+            seg_end(segPre);
             if (!exchange_classes_end()) break;  // the substep's one host synchronisation
             tmark("class sync");
             // sizes: what goes where, and this rank's layout after the sort
@@ -1686,6 +1780,7 @@ struct apbf_gpu_solver {
             const int ownB = (int)(lowG0 + lowG1), l1B = (int)lowG0;
             const int ownE = (int)(nLocal - hiG0 - hiG1), l1E = (int)(nLocal - hiG1);
             const int lowEnd = (int)(ownB + own2lo), highB = (int)(ownE - ownHi2);
+            seg_begin();  // segment 2: records, local sort, bucketing, lists
             std::vector<const void*> sp(G);
             std::vector<void*> rp(G);
             std::vector<size_t> sb(G), rb(G);
@@ -1752,6 +1847,7 @@ struct apbf_gpu_solver {
                                                                        ws.scene.p, radius, cfg.stab_iterations,
                                                                        s, ownB, ownE));
             LAUNCH_CHECK();
+            seg_end(segPost);
             tmark("sort+lists");
             ownB_ = ownB;
             ownE_ = ownE;
@@ -1762,6 +1858,9 @@ struct apbf_gpu_solver {
                 CK(cudaEventCreateWithFlags(&ev_halo_ready, cudaEventDisableTiming));
                 CK(cudaEventCreateWithFlags(&ev_halo_done, cudaEventDisableTiming));
             }
+            // segment 3: the iterations (the halo forks onto comm_stream and
+            // joins back inside the recording) and the finalize
+            seg_begin();
             for (int it = 1; it <= nMax; ++it) {
                 const float4* Pc = P[(it - 1) & 1];
                 float4* Pn = P[it & 1];
@@ -1814,6 +1913,7 @@ struct apbf_gpu_solver {
             if (nOwn > 0)
                 KL(k_finalize_owned<<<blocks(nOwn, 256), 256, 0, st>>>(nOwn, ownB, ctl, Pf, dst, src, dt, cap, s));
             LAUNCH_CHECK();
+            seg_end(segIter);
             n = nOwn;
             localPost[s] = n;
             cur ^= 1;  // the owned state now lives in the other set (src after the swap)
@@ -1843,6 +1943,7 @@ struct apbf_gpu_solver {
         const StateSet cs = set[cur].view();
         spanLo.ensure(kMaxRanks);
         spanHi.ensure(kMaxRanks);
+        seg_begin();
         KL(k_grid_reset<<<1, 1, 0, st>>>(ctl, 1));
         KL(k_aabb<<<blocks(n, kAabbBlock), kAabbBlock, 0, st>>>(n, cs.X, ctl, 1));
         KL(k_grid_reduce_pack<<<1, 1, 0, st>>>(ctl, 1, gridRed.p));
@@ -1862,6 +1963,7 @@ struct apbf_gpu_solver {
         KL(k_pack_pm<<<std::min(blocks(n, 256), 148 * 8), 256, 0, st>>>(sendIdx.p, cs.X, cs.XS, sendPM.p,
                                                                        destCountD.p, destStartD.p, clsRecv, G, g,
                                                                        recvPM.p, ownedFlag.p));
+        seg_end(segMetPre);
         if (!exchange_classes_end()) return;
         const int* sendC = hostCls;
         const int* recvC = hostCls + (size_t)G * kCls;
@@ -1877,6 +1979,7 @@ struct apbf_gpu_solver {
         }
         if (nM > n_capacity || nsend > send_capacity)  // cannot happen: see set_state_local
             fail(APBF_ERR_RUNTIME, "internal: slab metrics exchange larger than its worst-case capacity");
+        seg_begin();
         std::vector<const void*> sp(G);
         std::vector<void*> rp(G);
         std::vector<size_t> sb(G), rb(G);
@@ -1897,6 +2000,7 @@ struct apbf_gpu_solver {
         T.allreduce(&ctl->rho_sum, 1, RType::F64, ROp::Sum, st);
         T.allreduce(&ctl->rho_min_ord, 1, RType::I32, ROp::Min, st);
         T.allreduce(&ctl->rho_max_ord, 1, RType::I32, ROp::Max, st);
+        seg_end(segMetPost);
     }
 
     void frame_dist(bool assign_lod, const apbf_camera* cam, const apbf_lod_config* lod, int frame_index,

@@ -44,6 +44,10 @@ struct Transport {
     // Host all-to-all of one int64 per destination, ordered on `st` (returns
     // once recv is filled: the solver stream is synchronised).
     virtual void alltoall_counts(const long long* send, long long* recv, cudaStream_t st) = 0;
+    // True when allreduce/alltoallv only enqueue work on `st` (no host
+    // synchronisation), so they can be recorded into a CUDA graph by stream
+    // capture.
+    virtual bool capturable() const { return false; }
 };
 
 template <class T>
@@ -229,6 +233,7 @@ struct NcclTransport final : Transport {
     void* scratch = nullptr;
     int rank() const override { return r_; }
     int size() const override { return g_; }
+    bool capturable() const override { return true; }  // NCCL supports stream capture
 
     static int nccl_type(RType t) {  // ncclInt32 2, ncclUint32 3, ncclInt64 4, ncclFloat64 8
         return t == RType::I32 ? 2 : t == RType::U32 ? 3 : t == RType::I64 ? 4 : 8;

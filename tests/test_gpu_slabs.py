@@ -90,23 +90,68 @@ def test_slabs_report_numerical_error_like_single_gpu():
     assert (e1.value.pass_, e1.value.particle) == (e2.value.pass_, e2.value.particle) == ("predict", 23)
 
 
-def test_nccl_transport_single_rank_matches_plain_solver():
+@pytest.mark.parametrize("mode,seg_graphs", [("dtc", "1"), ("dtvs", "1"), ("pbf", "1"), ("dtc", "0")])
+def test_nccl_transport_single_rank_matches_plain_solver(monkeypatch, mode, seg_graphs):
     """The NCCL transport (dlopen'ed libnccl, ncclCommInitRank, all-reduce)
-    with a 1-rank communicator runs the slab frame and must equal Solver."""
+    with a 1-rank communicator runs the slab frame and must equal Solver.
+    With NCCL the slab frame records its segments into CUDA graphs and
+    updates them every substep (APBF_SLAB_GRAPHS=0: eager)."""
     from paper_1608_04721_b200.slab import SlabSolver, nccl_unique_id
+    monkeypatch.setenv("APBF_SLAB_GRAPHS", seg_graphs)
     spec = S.build_scenario("dam_break", 8000 / 216000)
-    spec.lod.model = LodModel.DTC
+    if mode == "pbf":
+        spec.solver.mode = SolverMode.PBF
+    else:
+        spec.lod.model = LodModel.DTC if mode == "dtc" else LodModel.DTVS
     one = Solver(spec.solver, spec.scene)
     nc = SlabSolver(spec.solver, spec.scene, 0, 1, nccl_unique_id())
     a = S.make_state(spec, 1)
     b = a.copy()
     one.upload(a)
     nc.upload_slice(b, b.count())
+    for f in range(6):
+        sa = one.step_frame_resident(spec.camera, spec.lod, f)
+        sb = nc.step_frame_resident(spec.camera, spec.lod, f)
+        assert (sa.total_iterations, sa.contacts, sa.min_density_pct, sa.max_density_pct) == \
+               (sb.total_iterations, sb.contacts, sb.min_density_pct, sb.max_density_pct), f
+        assert sa.avg_density_pct == pytest.approx(sb.avg_density_pct, rel=1e-12)
+    one.download(a)
+    nc.download(b)
+    for k in FIELDS:
+        assert np.array_equal(getattr(a, k), getattr(b, k)), k
+
+
+def test_nccl_recorded_segments_survive_a_failed_frame():
+    """A frame that aborts inside a recorded segment (NaN found in predict)
+    raises, keeps the start state, and the next frames still run through the
+    recorded segments and match the plain solver."""
+    from paper_1608_04721_b200.slab import SlabSolver, nccl_unique_id
+    spec = S.build_scenario("dam_break", 8000 / 216000)
+    spec.lod.model = LodModel.DTC
+    nc = SlabSolver(spec.solver, spec.scene, 0, 1, nccl_unique_id())
+    one = Solver(spec.solver, spec.scene)
+    good = S.make_state(spec, 1)
+    nc.upload_slice(good.copy(), good.count())
+    nc.step_frame_resident(spec.camera, spec.lod, 0)  # segments recorded once
+    bad = good.copy()
+    bad.v[100, 1] = np.nan
+    nc.upload_slice(bad, bad.count())
+    with pytest.raises(NumericalError):
+        nc.step_frame_resident(spec.camera, spec.lod, 1)
+    out = bad.copy()
+    for k in FIELDS:
+        getattr(out, k)[...] = 0
+    nc.download(out)
+    for k in FIELDS:
+        assert np.array_equal(getattr(out, k), getattr(bad, k), equal_nan=True), k
+    a, b = good.copy(), good.copy()
+    one.upload(a)
+    nc.upload_slice(b, b.count())
     for f in range(3):
         sa = one.step_frame_resident(spec.camera, spec.lod, f)
         sb = nc.step_frame_resident(spec.camera, spec.lod, f)
         assert (sa.total_iterations, sa.contacts, sa.min_density_pct) == \
-               (sb.total_iterations, sb.contacts, sb.min_density_pct)
+               (sb.total_iterations, sb.contacts, sb.min_density_pct), f
     one.download(a)
     nc.download(b)
     for k in FIELDS:
