@@ -1488,7 +1488,7 @@ struct apbf_gpu_solver {
             ws.rays.ensure(px);
             ws.raysa.ensure(px);
         }
-        seg_begin();  // (buffers sized above: the recording allocates nothing)
+        seg_begin(segLod);  // (buffers sized above: the recording allocates nothing)
         if (dtvs) {
             const CamFrame f = make_frame(cam);
             KL(k_splat_prep<<<blocks((long long)px, 256), 256, 0, st>>>(f, ws.depth.p, ws.rays.p, ws.raysa.p));
@@ -1573,8 +1573,15 @@ struct apbf_gpu_solver {
     // eager ones.  The loopback transport synchronises on the host inside its
     // collectives, so it runs the same code eagerly.  APBF_SLAB_GRAPHS=0 (or
     // APBF_GRAPHS=0, or APBF_SLAB_TRACE) records nothing.
+    // A segment whose recordings keep changing topology (every update fails
+    // and re-instantiates while the GPU waits) goes back to eager launches
+    // after kSegMaxFails consecutive failures.
+    static constexpr int kSegMaxFails = 8;
     struct SegGraph {
         cudaGraphExec_t exec = nullptr;
+        bool active = false;  // this occurrence is being recorded
+        bool off = false;     // recording abandoned (kSegMaxFails)
+        int fails = 0;        // consecutive failed in-place updates
         SegGraph() = default;
         SegGraph(const SegGraph&) = delete;
         SegGraph& operator=(const SegGraph&) = delete;
@@ -1588,14 +1595,16 @@ struct apbf_gpu_solver {
         const char* e = std::getenv("APBF_SLAB_GRAPHS");
         return !(e && e[0] == '0');
     }();
-    void seg_begin() {
-        if (!seg_on) return;
+    void seg_begin(SegGraph& sg) {
+        sg.active = seg_on && !sg.off;
+        if (!sg.active) return;
         CK(cudaStreamBeginCapture(ws.stream, cudaStreamCaptureModeThreadLocal));
         capturing = true;
         g_segment_capture = true;
     }
     void seg_end(SegGraph& sg) {
-        if (!seg_on) return;
+        if (!sg.active) return;
+        sg.active = false;
         capturing = false;
         g_segment_capture = false;
         cudaGraph_t g = nullptr;
@@ -1606,6 +1615,9 @@ struct apbf_gpu_solver {
                 (void)cudaGetLastError();
                 cudaGraphExecDestroy(sg.exec);
                 sg.exec = nullptr;
+                if (++sg.fails >= kSegMaxFails) sg.off = true;  // (this occurrence still runs)
+            } else {
+                sg.fails = 0;
             }
         }
         cudaError_t e = cudaSuccess;
@@ -1616,6 +1628,7 @@ struct apbf_gpu_solver {
     }
     // An exception while recording: leave capture mode, drop the recording.
     void seg_cancel() {
+        for (SegGraph* sg : {&segLod, &segPre, &segPost, &segIter, &segMetPre, &segMetPost}) sg->active = false;
         if (!g_segment_capture) return;
         capturing = false;
         g_segment_capture = false;
@@ -1716,7 +1729,7 @@ struct apbf_gpu_solver {
             NvtxRange range("apbf slab substep");
             localPre[s] = n;
             StateSet src = set[cur].view(), dst = set[cur ^ 1].view();
-            seg_begin();  // segment 1: everything up to the host synchronisation
+            seg_begin(segPre);  // segment 1: everything up to the host synchronisation
             KL(k_substep_reset<<<1, 1, 0, st>>>(ctl));
             KL(k_predict<<<blocks(n, kAabbBlock), kAabbBlock, 0, st>>>(n, src.X, src.V, src.V, src.XS, src.XS, dt,
                                                       cfg.gravity[0], cfg.gravity[1], cfg.gravity[2], ctl, s));
@@ -1780,7 +1793,7 @@ struct apbf_gpu_solver {
             const int ownB = (int)(lowG0 + lowG1), l1B = (int)lowG0;
             const int ownE = (int)(nLocal - hiG0 - hiG1), l1E = (int)(nLocal - hiG1);
             const int lowEnd = (int)(ownB + own2lo), highB = (int)(ownE - ownHi2);
-            seg_begin();  // segment 2: records, local sort, bucketing, lists
+            seg_begin(segPost);  // segment 2: records, local sort, bucketing, lists
             std::vector<const void*> sp(G);
             std::vector<void*> rp(G);
             std::vector<size_t> sb(G), rb(G);
@@ -1860,7 +1873,7 @@ struct apbf_gpu_solver {
             }
             // segment 3: the iterations (the halo forks onto comm_stream and
             // joins back inside the recording) and the finalize
-            seg_begin();
+            seg_begin(segIter);
             for (int it = 1; it <= nMax; ++it) {
                 const float4* Pc = P[(it - 1) & 1];
                 float4* Pn = P[it & 1];
@@ -1943,7 +1956,7 @@ struct apbf_gpu_solver {
         const StateSet cs = set[cur].view();
         spanLo.ensure(kMaxRanks);
         spanHi.ensure(kMaxRanks);
-        seg_begin();
+        seg_begin(segMetPre);
         KL(k_grid_reset<<<1, 1, 0, st>>>(ctl, 1));
         KL(k_aabb<<<blocks(n, kAabbBlock), kAabbBlock, 0, st>>>(n, cs.X, ctl, 1));
         KL(k_grid_reduce_pack<<<1, 1, 0, st>>>(ctl, 1, gridRed.p));
@@ -1979,7 +1992,7 @@ struct apbf_gpu_solver {
         }
         if (nM > n_capacity || nsend > send_capacity)  // cannot happen: see set_state_local
             fail(APBF_ERR_RUNTIME, "internal: slab metrics exchange larger than its worst-case capacity");
-        seg_begin();
+        seg_begin(segMetPost);
         std::vector<const void*> sp(G);
         std::vector<void*> rp(G);
         std::vector<size_t> sb(G), rb(G);
