@@ -216,6 +216,10 @@ struct NcclUniqueIdT {
 
 struct NcclTransport final : Transport {
     NcclTransport(int rank, int nranks, const unsigned char id[128]) : r_(rank), g_(nranks) {
+        // The slab frame re-records its segments (with NCCL calls inside)
+        // every substep with new sizes: no user-buffer registration per
+        // recording (unless the user asks for it).
+        setenv("NCCL_GRAPH_REGISTER", "0", 0);
         NcclApi& api = NcclApi::get();
         NcclUniqueIdT uid;
         std::memcpy(uid.internal, id, 128);
