@@ -19,10 +19,7 @@
 // CTA size of the passes that fold an AABB into the control block (predict,
 // aabb): one block-reduced atomic per coordinate bound per CTA, so large
 // CTAs (predict 28 -> 18 us, aabb 18 -> 11 us per 1M-particle launch, ncu)
-#ifndef APBF_AABB_BLOCK
-#define APBF_AABB_BLOCK 1024
-#endif
-static constexpr int kAabbBlock = APBF_AABB_BLOCK;
+static constexpr int kAabbBlock = 1024;
 
 #include <memory>
 #include <functional>
