@@ -295,7 +295,8 @@ struct alignas(64) Rec {
 // Records for the other ranks, sized on the device (enqueued ahead of the
 // substep's host synchronisation): destination q's segment starts at
 // destStart[q] and holds destCount[q] records; the rank's own segment g is
-// skipped (k_gather_self).  Grid-stride over the records that leave.
+// skipped: the local sort reads it in place (SelfMap).  Grid-stride over the
+// records that leave.
 __global__ void k_pack_recs(const int* __restrict__ idx, StateSet s, Rec* __restrict__ out,
                             const int* __restrict__ destCount, const int* __restrict__ destStart, int G, int g) {
     const int total = destStart[G - 1] + destCount[G - 1];
@@ -333,26 +334,6 @@ __global__ void k_unpack_recs(int cnt, const Rec* __restrict__ in, StateSet d, i
     d.W[k] = r.w;
     d.L[k] = r.lam;
     d.LV[k] = r.lv;
-}
-
-// The particles a rank keeps (its own exchange segment): straight from the
-// old state into their slots of the new local set, no record round trip.
-// Sized on the device: destCount[g] particles at destStart[g] of idx, placed
-// after the records of ranks q < g (the exchanged class totals recvCls[q * kCls]).
-__global__ void k_gather_self(const int* __restrict__ idx, StateSet from, StateSet to,
-                              const int* __restrict__ destCount, const int* __restrict__ destStart,
-                              const int* __restrict__ recvCls, int g) {
-    const int k = blockIdx.x * blockDim.x + threadIdx.x;
-    if (k >= destCount[g]) return;
-    int off = 0;
-    for (int q = 0; q < g; ++q) off += recvCls[q * kCls];
-    const int i = idx[destStart[g] + k];
-    to.X[off + k] = from.X[i];
-    to.V[off + k] = from.V[i];
-    to.XS[off + k] = from.XS[i];
-    to.W[off + k] = from.W[i];
-    to.L[off + k] = from.L[i];
-    to.LV[off + k] = from.LV[i];
 }
 
 // One all-reduce instead of three for the substep's grid: [~abort, lo(3),

@@ -207,13 +207,14 @@ struct Workspace {
     // ownLo/ownHi (slab mode, device pointers): contacts of the owned layers
     // only; params = false when the caller already ran k_grid_params for g.
     void run_grid(int g, const float4* P, int n, float h, float pad, bool contacts, float radius,
-                  const int* ownLo = nullptr, const int* ownHi = nullptr, bool params = true) {
+                  const int* ownLo = nullptr, const int* ownHi = nullptr, bool params = true,
+                  SelfMap self = SelfMap{}) {
         ensure_cells();
         ensure_particles(n);
         if (params) KL(k_grid_params<<<1, 1, 0, stream>>>(ctl.p, g, h, pad));
         KL(k_zero_cells<<<4 * 148, 256, 0, stream>>>(ctl.p, g, cellCount.p));
         KL(k_cell_keys<<<blocks(n, 256), 256, 0, stream>>>(n, P, ctl.p, g, h, cellCount.p, key.p, slot.p,
-                                                        scene.p, radius, contacts ? 1 : 0, ownLo, ownHi));
+                                                        scene.p, radius, contacts ? 1 : 0, ownLo, ownHi, self));
         KL(k_scan_reduce<<<kScanGrid, kScanBlock, 0, stream>>>(ctl.p, g, cellCount.p, partial.p));
         KL(k_scan_partials<<<1, kScanBlock, 0, stream>>>(ctl.p, partial.p, kScanGrid));
         KL(k_scan_apply<<<kScanGrid, kScanBlock, 0, stream>>>(ctl.p, g, cellCount.p, partial.p));
@@ -411,8 +412,9 @@ struct apbf_gpu_solver {
     // buffers the second substep's reorder fills only afterwards), so a
     // list-overflow retry restarts from it without a backup copy; successive
     // frames rotate through the sets (one cached graph per start set).  The
-    // slab path alternates set[0]/set[1] and keeps its retry copy in set[2].
-    SetBufs set[3];
+    // slab path keeps a rank's state in set[0] or set[1], receives records into
+    // the other, sorts into set[3] and keeps its retry copy in set[2].
+    SetBufs set[4];  // set[3]: slab mode's sorted local set
     int cur = 0;
     DBuf<float4> PB;
     DBuf<float4> PL;  // (x*, lambda) published by the lambda pass for the delta-p gathers
@@ -1413,6 +1415,7 @@ struct apbf_gpu_solver {
         // segment must not allocate (g_segment_capture)
         const long long tilesMax = (n_capacity + kTileSize - 1) / kTileSize;
         destTile.ensure((size_t)std::max(G, 1) * (size_t)std::max<long long>(tilesMax, 1));
+        set[3].ensure((size_t)n_capacity);
         ws.ensure_cells();
         ws.ensure_particles((size_t)n_capacity);
         if (G > 1) ensure_set_b();
@@ -1725,7 +1728,9 @@ struct apbf_gpu_solver {
         for (int s = 0; s < cfg.substeps; ++s) {
             NvtxRange range("apbf slab substep");
             localPre[s] = n;
-            StateSet src = set[cur].view(), dst = set[cur ^ 1].view();
+            // src: this rank's state (old, then new after the finalize); rec:
+            // the unsorted local set the records land in; dst: the sorted set
+            StateSet src = set[cur].view(), rec = set[cur ^ 1].view(), dst = set[3].view();
             seg_begin(segPre);  // segment 1: everything up to the host synchronisation
             KL(k_substep_reset<<<1, 1, 0, st>>>(ctl));
             KL(k_predict<<<blocks(n, kAabbBlock), kAabbBlock, 0, st>>>(n, src.X, src.V, src.V, src.XS, src.XS, dt,
@@ -1751,14 +1756,12 @@ struct apbf_gpu_solver {
             tmark("pre-exchange");
             exchange_classes_begin(T, kCls);
             // device-sized, ahead of the host synchronisation: expansion by
-            // destination, records for the other ranks, and this rank's own
-            // segment straight from the old state into the new local set
+            // destination and the records for the other ranks (this rank's
+            // own segment stays in the old state: SelfMap)
             expand_dest(G);
             if (G > 1)
                 KL(k_pack_recs<<<std::min(blocks(n, 256), 148 * 8), 256, 0, st>>>(sendIdx.p, src, sendRec.p,
                                                                                  destCountD.p, destStartD.p, G, g));
-            KL(k_gather_self<<<blocks(n, 256), 256, 0, st>>>(sendIdx.p, src, dst, destCountD.p, destStartD.p,
-                                                            clsRecv, g));
             seg_end(segPre);
             if (!exchange_classes_end()) break;  // the substep's one host synchronisation
             tmark("class sync");
@@ -1803,20 +1806,25 @@ struct apbf_gpu_solver {
             T.alltoallv(sp.data(), sb.data(), rp.data(), rb.data(), st);
             const int nL = (int)nLocal;
             if (nL > sendCnt[g])
-                KL(k_unpack_recs<<<blocks(nL, 256), 256, 0, st>>>(nL, recvRec.p, dst, (int)roff[g],
+                KL(k_unpack_recs<<<blocks(nL, 256), 256, 0, st>>>(nL, recvRec.p, rec, (int)roff[g],
                                                                 (int)(roff[g] + sendCnt[g])));
-            // the new local set is dst; the old state set is free and becomes the
-            // sorted set the iterations run on
-            std::swap(src, dst);
+            // the unsorted local set: rec, except its own segment [roff_g,
+            // roff_g + sendCnt_g), which is read from the old state
+            SelfMap self;
+            self.idx = sendIdx.p + sendStart[g];
+            self.off = (int)roff[g];
+            self.cnt = (int)sendCnt[g];
+            self.from = src;
             tmark("exchange");
             // local stable sort by global cell == global order restricted
             // (contacts of the owned layers counted on the way; grid params
             // already set for this grid above)
-            ws.run_grid(0, src.XS, nL, cfg.h, cfg.h, scene.n > 0, radius, zRange.p + g, zRange.p + G + g, false);
+            ws.run_grid(0, rec.XS, nL, cfg.h, cfg.h, scene.n > 0, radius, zRange.p + g, zRange.p + G + g, false,
+                        self);
             const int tilesL = std::max(1, (nL + kTileSize - 1) / kTileSize);
             const int smemG = (nMax + 1) * (int)sizeof(int);
-            KL(k_gather<<<tilesL, kTileThreads, smemG, st>>>(nL, ctl, ws.perm.p, src, dst, nMax, tilesL,
-                                                           tileCount.p));
+            KL(k_gather<<<tilesL, kTileThreads, smemG, st>>>(nL, ctl, ws.perm.p, rec, dst, nMax, tilesL,
+                                                           tileCount.p, 3, self));
             const int nOwn = ownE - ownB;
             // iteration order over owned + layer-1 ghosts (lambda is computed
             // redundantly for the latter), outer ghosts never active.  With
@@ -1926,7 +1934,7 @@ struct apbf_gpu_solver {
             seg_end(segIter);
             n = nOwn;
             localPost[s] = n;
-            cur ^= 1;  // the owned state now lives in the other set (src after the swap)
+            // (the new state is back in set[cur], which the old state was read from)
             tmark("finalize+copy");
         }
         CK(cudaEventRecord(ev[5], st));
@@ -2019,7 +2027,7 @@ struct apbf_gpu_solver {
         const int G = T.size(), g = T.rank();
         if (G > kMaxRanks) fail(APBF_ERR_INVALID_ARGUMENT, "too many slab ranks");
         if (observer) fail(APBF_ERR_INVALID_ARGUMENT, "iteration observer is not available with slab decomposition");
-        if (cur == 2) {  // left there by single-rank frames: the slab path alternates 0/1
+        if (cur == 2) {  // left there by single-rank frames: the slab path uses 0/1 (and 3)
             copy_set(set[0], set[2]);
             cur = 0;
         }
