@@ -1640,9 +1640,9 @@ struct apbf_gpu_solver {
 
     // Split in two: exchange_classes_begin enqueues the exchange and the
     // reads and records ev_cls; the caller then enqueues the device-sized
-    // work that does not need the host (the destination expansion, the
-    // record pack, the self gather) so that the GPU keeps running while the
-    // host waits in exchange_classes_end.
+    // work that does not need the host (the destination expansion and the
+    // record pack) so that the GPU keeps running while the host waits in
+    // exchange_classes_end.
     cudaEvent_t ev_cls = nullptr;
     void exchange_classes_begin(Transport& T, int ncls) {
         const int G = T.size(), g = T.rank();
