@@ -642,6 +642,23 @@ struct apbf_gpu_solver {
     // (fast_pair_coef), outside the bitwise contract
     bool fast_math = false;
 
+    // A solver pass with programmatic stream serialization (pdl_wait in the
+    // kernel): its launch overlaps the previous pass's tail.
+    template <typename... KArgs, typename... Args>
+    void launch_pdl(void (*k)(KArgs...), int grid, int block, cudaStream_t st, Args... args) {
+        cudaLaunchConfig_t lc = {};
+        lc.gridDim = dim3((unsigned)grid);
+        lc.blockDim = dim3((unsigned)block);
+        lc.dynamicSmemBytes = 0;
+        lc.stream = st;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[0].val.programmaticStreamSerializationAllowed = 1;
+        lc.attrs = attr;
+        lc.numAttrs = 1;
+        CK(cudaLaunchKernelEx(&lc, k, static_cast<KArgs>(args)...));
+        ++g_launches;
+    }
     // which: 1 the lambda pass, 2 the delta-p pass, 3 both
     template <bool kZ, bool kF>
     void launch_pair_t(int it, int s, const float4* Pc, float4* Pn, const StateSet& dst,
@@ -651,24 +668,26 @@ struct apbf_gpu_solver {
         constexpr int B = kLambdaThreads, K = kBatch, D = kDeltapThreads;
         const int sb = blocks(n_iter, B), sd = blocks(n_iter, D);
         // inverse-mass specialisations (w_mode, checked at upload)
+        auto lam = [&](auto kern) {
+            launch_pdl(kern, sb, B, st, n_iter, it, ctl, (const int*)activeCount.p, (const int*)order.p, Pc,
+                       (const float*)dst.W, dst.L, (const int*)nbr.p, (const int*)nbrCount.p,
+                       (const long long*)groupBase.p, sc, s, ownB_, ownE_, PL.p);
+        };
+        // inverse-mass specialisations (w_mode, checked at upload)
         if (!(which & 1)) {
         } else if (w_mode == 2)
-            KL(k_lambda<B, K, kZ, 2, kF><<<sb, B, 0, st>>>(n_iter, it, ctl, activeCount.p, order.p, Pc, dst.W,
-                                                          dst.L, nbr.p, nbrCount.p, groupBase.p, sc, s, ownB_,
-                                                          ownE_, PL.p));
+            lam(k_lambda<B, K, kZ, 2, kF>);
         else if (w_mode == 1)
-            KL(k_lambda<B, K, kZ, 1, kF><<<sb, B, 0, st>>>(n_iter, it, ctl, activeCount.p, order.p, Pc, dst.W,
-                                                          dst.L, nbr.p, nbrCount.p, groupBase.p, sc, s, ownB_,
-                                                          ownE_, PL.p));
+            lam(k_lambda<B, K, kZ, 1, kF>);
         else
-            KL(k_lambda<B, K, kZ, 0, kF><<<sb, B, 0, st>>>(n_iter, it, ctl, activeCount.p, order.p, Pc, dst.W,
-                                                          dst.L, nbr.p, nbrCount.p, groupBase.p, sc, s, ownB_,
-                                                          ownE_, PL.p));
+            lam(k_lambda<B, K, kZ, 0, kF>);
         if (tslot >= 0) rec(kt_ev[tslot][1]);
         if (which & 2)
-            KL(k_deltap_apply<kZ, D, K, kF><<<sd, D, 0, st>>>(
-                n_iter, it, ctl, activeCount.p, order.p, Pc, Pn, dst.W, dst.L, dst.LV, nbr.p, nbrCount.p,
-                groupBase.p, ws.scene.p, sc, s, ownB_, ownE_, PL.p));
+            launch_pdl(k_deltap_apply<kZ, D, K, kF>, sd, D, st, n_iter, it, ctl, (const int*)activeCount.p,
+                       (const int*)order.p, Pc, Pn, (const float*)dst.W, (const float*)dst.L,
+                       (const int*)dst.LV, (const int*)nbr.p, (const int*)nbrCount.p,
+                       (const long long*)groupBase.p, (const Scene*)ws.scene.p, sc, s, ownB_, ownE_,
+                       (const float4*)PL.p);
     }
 
     // The list build and the residual pass.
