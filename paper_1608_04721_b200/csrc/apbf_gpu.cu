@@ -76,6 +76,27 @@ static unsigned long long g_launches = 0;
         ++g_launches;    \
     } while (0)
 
+// A kernel launched with programmatic stream serialization (it starts with
+// pdl_wait(), apbf_device.cuh): its launch may overlap the predecessor's tail
+// in the stream (also inside a captured graph, as a programmatic edge).  Only
+// kernels whose first statement is pdl_wait() may be launched this way.
+template <typename... KArgs, typename... Args>
+static void launch_pdl(void (*k)(KArgs...), unsigned grid, unsigned block, size_t smem, cudaStream_t st,
+                       Args... args) {
+    cudaLaunchConfig_t lc = {};
+    lc.gridDim = dim3(grid);
+    lc.blockDim = dim3(block);
+    lc.dynamicSmemBytes = smem;
+    lc.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    lc.attrs = attr;
+    lc.numAttrs = 1;
+    CK(cudaLaunchKernelEx(&lc, k, static_cast<KArgs>(args)...));
+    ++g_launches;
+}
+
 int32_t to_err(const ApiError& e, apbf_error* out) {
     if (out) {
         out->code = e.code;
@@ -211,18 +232,18 @@ struct Workspace {
                   SelfMap self = SelfMap{}) {
         ensure_cells();
         ensure_particles(n);
-        if (params) KL(k_grid_params<<<1, 1, 0, stream>>>(ctl.p, g, h, pad));
-        KL(k_zero_cells<<<4 * 148, 256, 0, stream>>>(ctl.p, g, cellCount.p));
-        KL(k_cell_keys<<<blocks(n, 256), 256, 0, stream>>>(n, P, ctl.p, g, h, cellCount.p, key.p, slot.p,
-                                                        scene.p, radius, contacts ? 1 : 0, ownLo, ownHi, self));
-        KL(k_scan_reduce<<<kScanGrid, kScanBlock, 0, stream>>>(ctl.p, g, cellCount.p, partial.p));
-        KL(k_scan_partials<<<1, kScanBlock, 0, stream>>>(ctl.p, partial.p, kScanGrid));
-        KL(k_scan_apply<<<kScanGrid, kScanBlock, 0, stream>>>(ctl.p, g, cellCount.p, partial.p));
-        KL(k_bucket_fill<<<blocks(n, 256), 256, 0, stream>>>(n, ctl.p, key.p, slot.p, cellCount.p,
-                                                          bucket.p));
-        KL(k_stable_rank<<<blocks(n, 256), 256, 0, stream>>>(n, ctl.p, key.p, slot.p, cellCount.p, bucket.p,
-                                                          perm.p, heavy.p));
-        KL(k_heavy_sort<<<148, kHeavyThreads, 0, stream>>>(n, ctl.p, heavy.p, cellCount.p, bucket.p, perm.p));
+        if (params) launch_pdl(k_grid_params, (unsigned)(1), 1, 0, stream, ctl.p, g, h, pad);
+        launch_pdl(k_zero_cells, (unsigned)(4 * 148), 256, 0, stream, ctl.p, g, cellCount.p);
+        launch_pdl(k_cell_keys, (unsigned)(blocks(n, 256)), 256, 0, stream, n, P, ctl.p, g, h, cellCount.p, key.p, slot.p,
+                                                        scene.p, radius, contacts ? 1 : 0, ownLo, ownHi, self);
+        launch_pdl(k_scan_reduce, (unsigned)(kScanGrid), kScanBlock, 0, stream, ctl.p, g, cellCount.p, partial.p);
+        launch_pdl(k_scan_partials, (unsigned)(1), kScanBlock, 0, stream, ctl.p, partial.p, kScanGrid);
+        launch_pdl(k_scan_apply, (unsigned)(kScanGrid), kScanBlock, 0, stream, ctl.p, g, cellCount.p, partial.p);
+        launch_pdl(k_bucket_fill, (unsigned)(blocks(n, 256)), 256, 0, stream, n, ctl.p, key.p, slot.p, cellCount.p,
+                                                          bucket.p);
+        launch_pdl(k_stable_rank, (unsigned)(blocks(n, 256)), 256, 0, stream, n, ctl.p, key.p, slot.p, cellCount.p, bucket.p,
+                                                          perm.p, heavy.p);
+        launch_pdl(k_heavy_sort, (unsigned)(148), kHeavyThreads, 0, stream, n, ctl.p, heavy.p, cellCount.p, bucket.p, perm.p);
         LAUNCH_CHECK();
     }
 
@@ -642,23 +663,6 @@ struct apbf_gpu_solver {
     // (fast_pair_coef), outside the bitwise contract
     bool fast_math = false;
 
-    // A solver pass with programmatic stream serialization (pdl_wait in the
-    // kernel): its launch overlaps the previous pass's tail.
-    template <typename... KArgs, typename... Args>
-    void launch_pdl(void (*k)(KArgs...), int grid, int block, cudaStream_t st, Args... args) {
-        cudaLaunchConfig_t lc = {};
-        lc.gridDim = dim3((unsigned)grid);
-        lc.blockDim = dim3((unsigned)block);
-        lc.dynamicSmemBytes = 0;
-        lc.stream = st;
-        cudaLaunchAttribute attr[1];
-        attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-        attr[0].val.programmaticStreamSerializationAllowed = 1;
-        lc.attrs = attr;
-        lc.numAttrs = 1;
-        CK(cudaLaunchKernelEx(&lc, k, static_cast<KArgs>(args)...));
-        ++g_launches;
-    }
     // which: 1 the lambda pass, 2 the delta-p pass, 3 both
     template <bool kZ, bool kF>
     void launch_pair_t(int it, int s, const float4* Pc, float4* Pn, const StateSet& dst,
@@ -669,7 +673,7 @@ struct apbf_gpu_solver {
         const int sb = blocks(n_iter, B), sd = blocks(n_iter, D);
         // inverse-mass specialisations (w_mode, checked at upload)
         auto lam = [&](auto kern) {
-            launch_pdl(kern, sb, B, st, n_iter, it, ctl, (const int*)activeCount.p, (const int*)order.p, Pc,
+            launch_pdl(kern, sb, B, 0, st, n_iter, it, ctl, (const int*)activeCount.p, (const int*)order.p, Pc,
                        (const float*)dst.W, dst.L, (const int*)nbr.p, (const int*)nbrCount.p,
                        (const long long*)groupBase.p, sc, s, ownB_, ownE_, PL.p);
         };
@@ -683,7 +687,7 @@ struct apbf_gpu_solver {
             lam(k_lambda<B, K, kZ, 0, kF>);
         if (tslot >= 0) rec(kt_ev[tslot][1]);
         if (which & 2)
-            launch_pdl(k_deltap_apply<kZ, D, K, kF>, sd, D, st, n_iter, it, ctl, (const int*)activeCount.p,
+            launch_pdl(k_deltap_apply<kZ, D, K, kF>, sd, D, 0, st, n_iter, it, ctl, (const int*)activeCount.p,
                        (const int*)order.p, Pc, Pn, (const float*)dst.W, (const float*)dst.L,
                        (const int*)dst.LV, (const int*)nbr.p, (const int*)nbrCount.p,
                        (const long long*)groupBase.p, (const Scene*)ws.scene.p, sc, s, ownB_, ownE_,
@@ -698,9 +702,8 @@ struct apbf_gpu_solver {
                 nn, ws.ctl.p, order.p, dst.XS, ws.cellCount.p, cfg.h, cfg.h * cfg.h, nbr.p, nbrCount.p,
                 groupBase.p, nbrCap, activeCount.p + 1));
         else
-            KL(k_build_lists_direct<<<blocks(nn, kListThreads), kListThreads, 0, st>>>(
-                nn, ws.ctl.p, order.p, dst.XS, ws.cellCount.p, cfg.h, cfg.h * cfg.h, nbr.p, nbrCount.p,
-                groupBase.p, list_stride, activeCount.p + 1));
+            launch_pdl(k_build_lists_direct, (unsigned)(blocks(nn, kListThreads)), kListThreads, 0, st, nn, ws.ctl.p, order.p, dst.XS, ws.cellCount.p, cfg.h, cfg.h * cfg.h, nbr.p, nbrCount.p,
+                groupBase.p, list_stride, activeCount.p + 1);
     }
     void launch_residual(int nn, int it, const float4* Pn, const SolverConsts& sc, double* out, int oB,
                          int oE) {
@@ -859,7 +862,7 @@ struct apbf_gpu_solver {
             const int si = s == 0 ? sa : ((s & 1) ? sb : sc3);
             const int di = s == 0 ? sb : ((s & 1) ? sc3 : sb);
             StateSet src = set[si].view(), dst = set[di].view();
-            KL(k_substep_reset<<<1, 1, 0, st>>>(ctl));
+            launch_pdl(k_substep_reset, (unsigned)(1), 1, 0, st, ctl);
             // substep 0 predicts into the third set's V/x* (free until the
             // next substep's reorder), keeping the start set intact
             StateSet pin = src;
@@ -869,8 +872,8 @@ struct apbf_gpu_solver {
                 if (capturing) CK(cudaStreamWaitEvent(st, ev_vm, cudaEventWaitExternal));
                 else CK(cudaStreamWaitEvent(st, ev_vm, 0));
             }
-            KL(k_predict<<<blocks(n, kAabbBlock), kAabbBlock, 0, st>>>(n, src.X, src.V, pin.V, src.XS, pin.XS, dt,
-                                                      cfg.gravity[0], cfg.gravity[1], cfg.gravity[2], ctl, s));
+            launch_pdl(k_predict, (unsigned)(blocks(n, kAabbBlock)), kAabbBlock, 0, st, n, src.X, src.V, pin.V, src.XS, pin.XS, dt,
+                                                      cfg.gravity[0], cfg.gravity[1], cfg.gravity[2], ctl, s);
             ws.run_grid(0, pin.XS, n, cfg.h, cfg.h, scene.n > 0, radius);
             const int smemG = (nMax + 1) * (int)sizeof(int);
             if (s == 0) {
@@ -891,15 +894,15 @@ struct apbf_gpu_solver {
                                                                tileCount.p));
             }
             if (s == cfg.substeps - 1) rec(ev[7]);  // final storage order (overlapped download)
-            KL(k_level_scan<<<nMax + 1, 1024, 0, st>>>(ctl, numTiles, tileCount.p, levelCount.p));
-            KL(k_level_finish<<<1, 32, 0, st>>>(ctl, n, nMax, levelCount.p, activeCount.p, bucketStart.p));
-            KL(k_level_scatter<<<numTiles, kTileThreads, 9 * smemG, st>>>(n, ctl, dst.LV, nMax, numTiles,
-                                                                         tileCount.p, bucketStart.p, order.p));
+            launch_pdl(k_level_scan, (unsigned)(nMax + 1), 1024, 0, st, ctl, numTiles, tileCount.p, levelCount.p);
+            launch_pdl(k_level_finish, (unsigned)(1), 32, 0, st, ctl, n, nMax, levelCount.p, activeCount.p, bucketStart.p, 1);
+            launch_pdl(k_level_scatter, (unsigned)(numTiles), kTileThreads, 9 * smemG, st, n, ctl, dst.LV, nMax, numTiles,
+                                                                         tileCount.p, bucketStart.p, order.p);
             launch_build_lists(n, dst);
             if (S > 1)
-                KL(k_prestabilize<<<blocks(n, 256), 256, 0, st>>>(n, ctl, activeCount.p, S, order.p, dst.XS,
+                launch_pdl(k_prestabilize, (unsigned)(blocks(n, 256)), 256, 0, st, n, ctl, activeCount.p, S, order.p, dst.XS,
                                                                dst.X, ws.scene.p, radius, cfg.stab_iterations,
-                                                               s));
+                                                               s);
             LAUNCH_CHECK();
             mark(2);
             float4* P[2] = {dst.XS, PB.p};
@@ -945,8 +948,8 @@ struct apbf_gpu_solver {
             }
             mark(3);
             float4* Pf = P[lastIter & 1];
-            KL(k_finalize<<<blocks(n, 256), 256, 0, st>>>(n, ctl, Pf, dst.XS, dst.X, dst.V, dt, cap,
-                                                       Pf != dst.XS ? 1 : 0, s));
+            launch_pdl(k_finalize, (unsigned)(blocks(n, 256)), 256, 0, st, n, ctl, Pf, dst.XS, dst.X, dst.V, dt, cap,
+                                                       Pf != dst.XS ? 1 : 0, s);
             if (post_pass()) {  // opt-in XSPH / vorticity confinement (apbf_post.cuh)
                 const KernelConsts kc = make_kernel_consts(cfg.h);
                 KL(k_post_omega<<<blocks(n, 256), 256, 0, st>>>(n, ctl, order.p, dst.X, dst.V, nbr.p,
@@ -1751,15 +1754,15 @@ struct apbf_gpu_solver {
             // the unsorted local set the records land in; dst: the sorted set
             StateSet src = set[cur].view(), rec = set[cur ^ 1].view(), dst = set[3].view();
             seg_begin(segPre);  // segment 1: everything up to the host synchronisation
-            KL(k_substep_reset<<<1, 1, 0, st>>>(ctl));
-            KL(k_predict<<<blocks(n, kAabbBlock), kAabbBlock, 0, st>>>(n, src.X, src.V, src.V, src.XS, src.XS, dt,
-                                                      cfg.gravity[0], cfg.gravity[1], cfg.gravity[2], ctl, s));
+            launch_pdl(k_substep_reset, (unsigned)(1), 1, 0, st, ctl);
+            launch_pdl(k_predict, (unsigned)(blocks(n, kAabbBlock)), kAabbBlock, 0, st, n, src.X, src.V, src.V, src.XS, src.XS, dt,
+                                                      cfg.gravity[0], cfg.gravity[1], cfg.gravity[2], ctl, s);
             // global grid: AABB all-reduce (ordered ints), identical params
             // everywhere; the abort flag travels alongside
             KL(k_grid_reduce_pack<<<1, 1, 0, st>>>(ctl, 0, gridRed.p));
             T.allreduce(gridRed.p, 7, RType::I32, ROp::Min, st);
             KL(k_grid_reduce_unpack<<<1, 1, 0, st>>>(ctl, 0, gridRed.p));
-            KL(k_grid_params<<<1, 1, 0, st>>>(ctl, 0, cfg.h, cfg.h));
+            launch_pdl(k_grid_params, (unsigned)(1), 1, 0, st, ctl, 0, cfg.h, cfg.h);
             // slabs: equal-work split (sum of 1 + level per layer) of the
             // global histogram, computed on the device
             CK(cudaMemsetAsync(layerHist.p, 0, sizeof(int) * layer_cap, st));
@@ -1862,10 +1865,10 @@ struct apbf_gpu_solver {
                 KL(k_mask_level_tiles<<<tilesL, kTileThreads, smemG, st>>>(nL, ctl, dst.LV, b, e, xb, xe, LVo.p,
                                                                           nMax, tilesL, tileCount.p,
                                                                           total ? ownB : 0, total ? ownE : 0));
-                KL(k_level_scan<<<nMax + 1, 1024, 0, st>>>(ctl, tilesL, tileCount.p, levelCount.p));
-                KL(k_level_finish<<<1, 32, 0, st>>>(ctl, nL, nMax, levelCount.p, activeCount.p, bucketStart.p, 0));
-                KL(k_level_scatter<<<tilesL, kTileThreads, 9 * smemG, st>>>(nL, ctl, LVo.p, nMax, tilesL,
-                                                                           tileCount.p, bucketStart.p, order.p));
+                launch_pdl(k_level_scan, (unsigned)(nMax + 1), 1024, 0, st, ctl, tilesL, tileCount.p, levelCount.p);
+                launch_pdl(k_level_finish, (unsigned)(1), 32, 0, st, ctl, nL, nMax, levelCount.p, activeCount.p, bucketStart.p, 0);
+                launch_pdl(k_level_scatter, (unsigned)(tilesL), kTileThreads, 9 * smemG, st, nL, ctl, LVo.p, nMax, tilesL,
+                                                                           tileCount.p, bucketStart.p, order.p);
                 launch_build_lists(nL, dst);
             };
             if (split) {
@@ -1986,7 +1989,7 @@ struct apbf_gpu_solver {
         KL(k_grid_reduce_pack<<<1, 1, 0, st>>>(ctl, 1, gridRed.p));
         T.allreduce(gridRed.p, 7, RType::I32, ROp::Min, st);
         KL(k_grid_reduce_unpack<<<1, 1, 0, st>>>(ctl, 1, gridRed.p));
-        KL(k_grid_params<<<1, 1, 0, st>>>(ctl, 1, cfg.h, cfg.h));
+        launch_pdl(k_grid_params, (unsigned)(1), 1, 0, st, ctl, 1, cfg.h, cfg.h);
         KL(k_span_init<<<1, 32, 0, st>>>(G, spanLo.p, spanHi.p));
         KL(k_layer_minmax<<<blocks(n, 256), 256, 0, st>>>(n, cs.X, ctl, 1, cfg.h, spanLo.p + g, spanHi.p + g));
         T.allreduce(spanLo.p, G, RType::I32, ROp::Min, st);
