@@ -452,6 +452,7 @@ struct apbf_gpu_solver {
     bool phase_timing = false;
     float phase_ms[5] = {0, 0, 0, 0, 0};
     cudaEvent_t ev[8];
+    cudaEvent_t ev_lam = nullptr;  // the frame's last lambda pass is done (lambda final)
     apbf_iteration_observer observer = nullptr;
     void* observer_user = nullptr;
     // observer view of the in-flight state
@@ -501,6 +502,7 @@ struct apbf_gpu_solver {
         cap = cfg.velocity_cap > 0.0f ? cfg.velocity_cap : cfg.h / dt;
         S = cfg.stab_threshold > 0 ? cfg.stab_threshold : cfg.n_max;
         for (auto& e : ev) CK(cudaEventCreate(&e));
+        CK(cudaEventCreateWithFlags(&ev_lam, cudaEventDisableTiming));
         CK(cudaStreamCreateWithFlags(&lod_stream, cudaStreamNonBlocking));
         CK(cudaEventCreateWithFlags(&ev_lod_fork, cudaEventDisableTiming));
         CK(cudaEventCreateWithFlags(&ev_lod_join, cudaEventDisableTiming));
@@ -520,6 +522,7 @@ struct apbf_gpu_solver {
     ~apbf_gpu_solver() {
         drop_graph();
         for (auto& e : ev) cudaEventDestroy(e);
+        if (ev_lam) cudaEventDestroy(ev_lam);
         if (ev_x) cudaEventDestroy(ev_x);
         if (ev_vm) cudaEventDestroy(ev_vm);
         if (ev_inputs) cudaEventDestroy(ev_inputs);
@@ -531,6 +534,7 @@ struct apbf_gpu_solver {
         if (ev_halo_ready) cudaEventDestroy(ev_halo_ready);
         if (ev_halo_done) cudaEventDestroy(ev_halo_done);
         if (ev_cls) cudaEventDestroy(ev_cls);
+        if (ev_xdl) cudaEventDestroy(ev_xdl);
         if (hostCls) cudaFreeHost(hostCls);
     }
 
@@ -927,7 +931,15 @@ struct apbf_gpu_solver {
                 float4* Pn = P[it & 1];
                 const int tslot = kernel_timing ? (int)kt_used++ : -1;
                 if (tslot >= 0) rec(kt_ev[tslot][0]);
-                launch_solver_pair(it, s, Pc, Pn, dst, sc, tslot);
+                if (s == cfg.substeps - 1 && it == nMax && !observer) {
+                    // lambda is final after the frame's last lambda pass: its
+                    // download may start under the last delta-p and finalize
+                    launch_solver_pair(it, s, Pc, Pn, dst, sc, tslot, 1);
+                    rec(ev_lam);
+                    launch_solver_pair(it, s, Pc, Pn, dst, sc, -1, 2);
+                } else {
+                    launch_solver_pair(it, s, Pc, Pn, dst, sc, tslot);
+                }
                 if (tslot >= 0) rec(kt_ev[tslot][2]);
                 if (cfg.record_residuals) {
                     CK(cudaMemsetAsync(resid.p + (size_t)s * nMax + (it - 1), 0, sizeof(double), st));
@@ -946,6 +958,7 @@ struct apbf_gpu_solver {
                     in_iteration = false;
                 }
             }
+            if (s == cfg.substeps - 1 && observer) rec(ev_lam);
             mark(3);
             float4* Pf = P[lastIter & 1];
             launch_pdl(k_finalize, (unsigned)(blocks(n, 256)), 256, 0, st, n, ctl, Pf, dst.XS, dst.X, dst.V, dt, cap,
@@ -991,6 +1004,7 @@ struct apbf_gpu_solver {
         float *x, *xs, *v, *mass, *inv_mass, *lambda;
         int32_t* level;
         bool queued;
+        bool xs_from_x = false;  // x* is filled on the host from x (equal after finalize)
     };
     // The caller's x*, lambda and level as passed in (stepFrame overwrites
     // them before reading them, so the frame never needs them): uploaded raw
@@ -1062,13 +1076,37 @@ struct apbf_gpu_solver {
         if (o.mass) CK(cudaMemcpyAsync(o.mass, d + 9LL * n, n1, cudaMemcpyDeviceToHost, st));
         if (o.inv_mass) CK(cudaMemcpyAsync(o.inv_mass, d + 10LL * n, n1, cudaMemcpyDeviceToHost, st));
         if (o.level) CK(cudaMemcpyAsync(o.level, d + 12LL * n, n1, cudaMemcpyDeviceToHost, st));
+        // lambda straight from the final set once the last lambda pass is done
+        CK(cudaStreamWaitEvent(st, ev_lam, 0));
+        if (o.lambda) CK(cudaMemcpyAsync(o.lambda, fin.L, n1, cudaMemcpyDeviceToHost, st));
         CK(cudaStreamWaitEvent(st, ev[5], 0));
         KL(k_pack_dynamic<<<blocks(n, 256), 256, 0, st>>>(n, fin, d));
         LAUNCH_CHECK();
         if (o.x) CK(cudaMemcpyAsync(o.x, d, n3, cudaMemcpyDeviceToHost, st));
-        if (o.xs) CK(cudaMemcpyAsync(o.xs, d + 3LL * n, n3, cudaMemcpyDeviceToHost, st));
+        // After finalize x* == x bit for bit (finalize sets x = x*,
+        // solver.hpp:347-356): x* is not read back a second time over PCIe
+        // but copied from x on the host while v and lambda arrive
+        // (finish_frame).
+        o.xs_from_x = o.x && o.xs;
+        if (o.xs_from_x) {
+            if (!ev_xdl) CK(cudaEventCreateWithFlags(&ev_xdl, cudaEventDisableTiming));
+            CK(cudaEventRecord(ev_xdl, st));
+        } else if (o.xs) {
+            CK(cudaMemcpyAsync(o.xs, d + 3LL * n, n3, cudaMemcpyDeviceToHost, st));
+        }
         if (o.v) CK(cudaMemcpyAsync(o.v, d + 6LL * n, n3, cudaMemcpyDeviceToHost, st));
-        if (o.lambda) CK(cudaMemcpyAsync(o.lambda, d + 11LL * n, n1, cudaMemcpyDeviceToHost, st));
+    }
+    cudaEvent_t ev_xdl = nullptr;  // enqueue_download: x has reached the caller's array
+
+    // dst[0, m) = src[0, m) on the host, in parallel (page-locked caller
+    // arrays: one thread cannot saturate host memory bandwidth).
+    static void host_copy(float* dst, const float* src, size_t m) {
+        const long long chunks = 16, per = (long long)((m + chunks - 1) / chunks);
+#pragma omp parallel for schedule(static) num_threads(8)
+        for (long long c = 0; c < chunks; ++c) {
+            const long long b = c * per, e = std::min<long long>((long long)m, b + per);
+            if (b < e) std::memcpy(dst + b, src + b, sizeof(float) * (size_t)(e - b));
+        }
     }
 
     // A frame that failed after its overlapped download was queued: give the
@@ -1111,6 +1149,10 @@ struct apbf_gpu_solver {
             if (!copy_stream) CK(cudaStreamCreateWithFlags(&copy_stream, cudaStreamNonBlocking));
             enqueue_download(copy_stream, *host_out);
             host_out->queued = true;
+        }
+        if (host_out && host_out->queued && host_out->xs_from_x) {
+            CK(cudaEventSynchronize(ev_xdl));
+            host_copy(host_out->xs, host_out->x, 3 * (size_t)n);
         }
         CK(cudaStreamSynchronize(ws.stream));
         if (host_out && n > 0) CK(cudaStreamSynchronize(copy_stream));
