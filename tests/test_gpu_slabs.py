@@ -90,8 +90,9 @@ def test_slabs_report_numerical_error_like_single_gpu():
     assert (e1.value.pass_, e1.value.particle) == (e2.value.pass_, e2.value.particle) == ("predict", 23)
 
 
-@pytest.mark.parametrize("mode,seg_graphs", [("dtc", "1"), ("dtvs", "1"), ("pbf", "1"), ("dtc", "0")])
-def test_nccl_transport_single_rank_matches_plain_solver(monkeypatch, mode, seg_graphs):
+@pytest.mark.parametrize("mode,seg_graphs,frames", [("dtc", "1", 40), ("dtvs", "1", 6), ("pbf", "1", 6),
+                                                    ("dtc", "0", 6)])
+def test_nccl_transport_single_rank_matches_plain_solver(monkeypatch, mode, seg_graphs, frames):
     """The NCCL transport (dlopen'ed libnccl, ncclCommInitRank, all-reduce)
     with a 1-rank communicator runs the slab frame and must equal Solver.
     With NCCL the slab frame records its segments into CUDA graphs and
@@ -109,7 +110,7 @@ def test_nccl_transport_single_rank_matches_plain_solver(monkeypatch, mode, seg_
     b = a.copy()
     one.upload(a)
     nc.upload_slice(b, b.count())
-    for f in range(6):
+    for f in range(frames):  # (40 frames: 80 substeps of in-place segment updates)
         sa = one.step_frame_resident(spec.camera, spec.lod, f)
         sb = nc.step_frame_resident(spec.camera, spec.lod, f)
         assert (sa.total_iterations, sa.contacts, sa.min_density_pct, sa.max_density_pct) == \
