@@ -59,6 +59,9 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-fast", action="store_true", help="skip the fast-build (FMA) twin measurement")
     ap.add_argument("--cpu-frames", type=int, default=1, help="timed reference frames (cpu_baseline)")
+    ap.add_argument("--slab-check", action="store_true",
+                    help="run the N > 1 code path (8M tank, z-slab solver, strong-scaling t1, slab e2e) with one "
+                         "NCCL rank on one GPU: a check of that path, not a measurement the driver asks for")
     return ap.parse_args()
 
 
@@ -150,9 +153,14 @@ def ncu_warp_instructions(kernel: str):
         return None
 
 
+def slab_mode(args, world):
+    """The z-slab path: N > 1 GPUs, or --slab-check with one rank."""
+    return world > 1 or getattr(args, "slab_check", False)
+
+
 def bench_scenario(args, world):
     """C3 (1M ocean) on one GPU; C5 (8M tank, strong scaling) on N > 1."""
-    return args.scenario if world == 1 else "tank_8m"
+    return "tank_8m" if slab_mode(args, world) else args.scenario
 
 
 def make_config(spec, world, args):
@@ -162,7 +170,7 @@ def make_config(spec, world, args):
                         f"lod={spec.lod.model.name.lower()}, {spec.solver.substeps} substeps, "
                         "metrics pass included",
             "scenario_file": f"scenarios/{spec.name}.cfg", "seed": args.seed,
-            "parallelism": "single GPU" if world == 1 else
+            "parallelism": "single GPU" if not slab_mode(args, world) else
             f"{world} z-slabs (strong scaling of the fixed {n}-particle domain), NCCL migration+halo "
             "all-to-all per substep, x* halo per iteration",
             "l2": "inputs larger than L2 (~0.5 GB device state + scratch per frame)"}
@@ -350,17 +358,19 @@ def run_ours(args, world, rank, local, pg):
     from paper_1608_04721_b200.slab import SlabSolver, nccl_unique_id, slice_state
 
     torch.cuda.set_device(local)
+    slab = slab_mode(args, world)
     spec = S.build_scenario(bench_scenario(args, world))
     n_global = spec.particle_count()
     cam, lod = spec.camera, spec.lod
-    if world == 1:
+    if not slab:
         solver = Solver(spec.solver, spec.scene, device=local)
         state = S.make_state(spec, args.seed)
         solver.upload(state)
     else:
         # one process per GPU, NCCL communicator for the slab exchanges
         uid = [nccl_unique_id() if rank == 0 else None]
-        pg.broadcast_object_list(uid, src=0)
+        if pg is not None:
+            pg.broadcast_object_list(uid, src=0)
         solver = SlabSolver(spec.solver, spec.scene, rank, world, uid[0], device=local)
         state = slice_state(S.make_state(spec, args.seed), rank, world)
         solver.upload_slice(state, n_global)
@@ -404,7 +414,7 @@ def run_ours(args, world, rank, local, pg):
     # (the events sit between the kernels of the captured frame graph and cost
     # ~0.3 ms per frame, so the headline value comes from the clean region above)
     kt, ms_kt = None, None
-    if world == 1:
+    if not slab:
         solver.set_kernel_timing(True)
         for f in range(3):  # eager, capture, replay: the timed frames are graph replays
             solver.step_frame_resident(cam, lod, 1500 + f)
@@ -421,7 +431,7 @@ def run_ours(args, world, rank, local, pg):
 
     # ------- the fast build (apbf_gpu_set_fast_math), same frames, reported beside -------
     fast = None
-    if world == 1 and not args.no_fast:
+    if not slab and not args.no_fast:
         solver.set_fast_math(True)
         for f in range(3):
             solver.step_frame_resident(cam, lod, 1700 + f)
@@ -453,7 +463,7 @@ def run_ours(args, world, rank, local, pg):
 
     # ------- N > 1: the same fixed domain on ONE GPU (rank 0), for t1 / tN -------
     strong = None
-    if world > 1:
+    if slab:
         barrier(pg)
         if rank == 0:
             one = Solver(spec.solver, spec.scene, device=local)
@@ -481,10 +491,10 @@ def run_ours(args, world, rank, local, pg):
     e2e = None
     if not args.no_e2e:
         host = S.make_state(spec, args.seed)
-        if world > 1:
+        if slab:
             host = slice_state(host, rank, world)
         n_host = host.count()
-        cap = n_host if world == 1 else n_global + 4096  # a rank never holds more than all particles
+        cap = n_host if not slab else n_global + 4096  # a rank never holds more than all particles
 
         def pinned(shape, dtype):
             return torch.empty(shape, dtype=dtype, pin_memory=True).numpy()
@@ -504,7 +514,7 @@ def run_ours(args, world, rank, local, pg):
 
         def e2e_step(m, frame):
             st = view(m)
-            if world == 1:
+            if not slab:
                 # stepFrame(ParticleSet&) in one call (apbf_gpu_step_frame_host):
                 # upload the frame's inputs, step, write the reordered state back
                 return solver.step_frame(st, cam, lod, frame), m
@@ -555,7 +565,7 @@ def run_ours(args, world, rank, local, pg):
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": max(3, args.warmup), "ms_per_step": ms_max / args.steps,
-        "higher_is_better": True, "scaling": "weak" if world == 1 else "strong", "vs_baseline": None,
+        "higher_is_better": True, "scaling": "weak" if not slab else "strong", "vs_baseline": None,
         "dtype": "f32", "data": "synthetic",
         "config": make_config(spec, world, args),
         "steps_per_s": args.steps / (ms_max / 1e3),
@@ -569,9 +579,9 @@ def run_ours(args, world, rank, local, pg):
     }
     if strong is not None:
         line["strong_scaling"] = strong
-    if world == 1 and not args.no_e2e:
+    if not slab and not args.no_e2e:
         line["e2e_cpp"] = e2e_cpp(args)
-    if world == 1:
+    if not slab:
         sm_mhz = clk.get("sm_mhz") or 1965.0
         line["roofline"], line["roofline_fp32"] = rooflines(kt, ms_kt, entries / n_global, sm_mhz, hbm_peak,
                                                             peak_kind, args.steps, fma=False)

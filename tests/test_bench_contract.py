@@ -21,7 +21,7 @@ def bench():
 
 def args(**kw):
     a = argparse.Namespace(gpus=1, steps=20, warmup=5, impl="ours", scenario="ocean_1m", seed=1,
-                           no_cpu_baseline=False, no_e2e=False, no_fast=False, cpu_frames=1)
+                           no_cpu_baseline=False, no_e2e=False, no_fast=False, cpu_frames=1, slab_check=False)
     for k, v in kw.items():
         setattr(a, k, v)
     return a
@@ -31,6 +31,9 @@ def test_workload_per_gpu_count(bench):
     assert bench.bench_scenario(args(), 1) == "ocean_1m"
     for n in (2, 4, 8):
         assert bench.bench_scenario(args(gpus=n), n) == "tank_8m"
+    # --slab-check: the N > 1 path (tank, slab solver) with one rank
+    assert bench.bench_scenario(args(slab_check=True), 1) == "tank_8m"
+    assert bench.slab_mode(args(slab_check=True), 1) and not bench.slab_mode(args(), 1)
 
 
 def test_both_arms_print_the_same_config(bench):
