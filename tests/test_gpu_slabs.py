@@ -159,6 +159,30 @@ def test_nccl_recorded_segments_survive_a_failed_frame():
         assert np.array_equal(getattr(a, k), getattr(b, k)), k
 
 
+def test_nccl_slab_host_round_trip_matches_plain_host_frames():
+    """The N > 1 e2e path of bench.py on one rank: every frame uploads only the
+    frame's inputs (upload_slice(frame_inputs_only=True)), steps, and
+    downloads the reordered slice; the result equals the plain solver's host
+    stepFrame, bit for bit."""
+    from paper_1608_04721_b200.slab import SlabSolver, nccl_unique_id
+    spec = S.build_scenario("dam_break", 8000 / 216000)
+    spec.lod.model = LodModel.DTC
+    one = Solver(spec.solver, spec.scene)
+    nc = SlabSolver(spec.solver, spec.scene, 0, 1, nccl_unique_id())
+    a = S.make_state(spec, 1)
+    b = a.copy()
+    nc.upload_slice(b, b.count())  # full state once (levels etc.)
+    for f in range(4):
+        sa = one.step_frame(a, spec.camera, spec.lod, f)
+        nc.upload_slice(b, b.count(), frame_inputs_only=True)
+        sb = nc.step_frame_resident(spec.camera, spec.lod, f)
+        nc.download(b)
+        assert (sa.total_iterations, sa.contacts, sa.min_density_pct) == \
+               (sb.total_iterations, sb.contacts, sb.min_density_pct), f
+        for k in FIELDS:
+            assert np.array_equal(getattr(a, k), getattr(b, k)), (f, k)
+
+
 def test_failed_slab_frame_keeps_start_state():
     """All-or-nothing across ranks too: after a failing slab frame (NaN in one
     rank's slice, found in predict) every rank holds its frame-start state,
