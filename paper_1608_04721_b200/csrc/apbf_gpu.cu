@@ -355,27 +355,27 @@ void run_lod(Workspace& ws, const float4* X, int n, const apbf_camera& cam, cons
         ws.depth.ensure(px);
         ws.rays.ensure(px);
         ws.raysa.ensure(px);
-        KL(k_splat_prep<<<blocks((long long)px, 256), 256, 0, st>>>(f, ws.depth.p, ws.rays.p, ws.raysa.p));
-        KL(k_splat<<<blocks(n, 256), 256, 0, st>>>(n, X, radius, f, ws.depth.p, ws.rays.p, ws.raysa.p));
+        launch_pdl(k_splat_prep, (unsigned)(blocks((long long)px, 256)), 256, 0, st, f, ws.depth.p, ws.rays.p, ws.raysa.p);
+        launch_pdl(k_splat, (unsigned)(blocks(n, 256)), 256, 0, st, n, X, radius, f, ws.depth.p, ws.rays.p, ws.raysa.p);
         // each LOD pass counts its own visible sample (several per frame with cameras)
         CK(cudaMemsetAsync(&ws.ctl.p->sample_count, 0, sizeof(int), st));
-        KL(k_dtvs_gap<<<blocks(n, 256), 256, 0, st>>>(n, X, radius, f, ws.depth.p, ws.dist.p, ws.keys.p,
-                                                   ws.ctl.p));
+        launch_pdl(k_dtvs_gap, (unsigned)(blocks(n, 256)), 256, 0, st, n, X, radius, f, ws.depth.p, ws.dist.p, ws.keys.p,
+                                                   ws.ctl.p);
     } else {
-        KL(k_dtc_dist<<<blocks(n, 256), 256, 0, st>>>(n, X, cam.eye[0], cam.eye[1], cam.eye[2], ws.dist.p,
-                                                   ws.keys.p));
+        launch_pdl(k_dtc_dist, (unsigned)(blocks(n, 256)), 256, 0, st, n, X, cam.eye[0], cam.eye[1], cam.eye[2], ws.dist.p,
+                                                   ws.keys.p);
     }
     if (lod.auto_range) {
-        KL(k_rs_init<<<1, 1024, 0, st>>>(ws.rs.p, ws.ctl.p, n, dtvs ? 1 : 0));
+        launch_pdl(k_rs_init, (unsigned)(1), 1024, 0, st, ws.rs.p, ws.ctl.p, n, dtvs ? 1 : 0);
         const int hb = std::min(blocks(n, 256), 16 * 148);  // ~2 keys per thread: no load chain
         for (int pass = 0; pass < 3; ++pass) {
-            KL(k_rs_hist<<<hb, 256, 0, st>>>(n, ws.keys.p, ws.rs.p, pass));
-            KL(k_rs_select<<<1, 1024, 0, st>>>(ws.rs.p, pass));
+            launch_pdl(k_rs_hist, (unsigned)(hb), 256, 0, st, n, ws.keys.p, ws.rs.p, pass);
+            launch_pdl(k_rs_select, (unsigned)(1), 1024, 0, st, ws.rs.p, pass);
         }
     }
-    KL(k_lod_params<<<1, 1, 0, st>>>(ws.rs.p, ws.ctl.p, lod.auto_range, lod.d_min, lod.d_max, dtvs ? 1 : 0));
-    KL(k_lod_map<<<blocks(n, 256), 256, 0, st>>>(n, ws.ctl.p, ws.dist.p, ws.keys.p, dtvs ? 1 : 0, lod.n_min,
-                                              lod.n_max, LV));
+    launch_pdl(k_lod_params, (unsigned)(1), 1, 0, st, ws.rs.p, ws.ctl.p, lod.auto_range, lod.d_min, lod.d_max, dtvs ? 1 : 0);
+    launch_pdl(k_lod_map, (unsigned)(blocks(n, 256)), 256, 0, st, n, ws.ctl.p, ws.dist.p, ws.keys.p, dtvs ? 1 : 0, lod.n_min,
+                                              lod.n_max, LV);
     LAUNCH_CHECK();
 }
 
@@ -834,7 +834,7 @@ struct apbf_gpu_solver {
         rec(ev[0]);
         kt_used = 0;
         n_iter = n;
-        KL(k_frame_begin<<<1, 1, 0, st>>>(ctl));
+        launch_pdl(k_frame_begin, (unsigned)(1), 1, 0, st, ctl);
         // The LOD pass (APBF) reads only x and writes only the levels and its
         // own control fields; nothing before the first reorder reads levels.
         // So it forks onto lod_stream and runs beside the first substep's
@@ -888,14 +888,14 @@ struct apbf_gpu_solver {
             }
             if (s == 0 && lod_forked) {
                 // the fields now, the levels once the forked LOD pass joins
-                KL(k_gather<<<numTiles, kTileThreads, smemG, st>>>(n, ctl, ws.perm.p, pin, dst, nMax, numTiles,
-                                                               tileCount.p, 1));
+                launch_pdl(k_gather, (unsigned)(numTiles), kTileThreads, smemG, st, n, ctl, ws.perm.p, pin, dst, nMax, numTiles,
+                                                               tileCount.p, 1, SelfMap{});
                 CK(cudaStreamWaitEvent(st, ev_lod_join, 0));
-                KL(k_gather<<<numTiles, kTileThreads, smemG, st>>>(n, ctl, ws.perm.p, pin, dst, nMax, numTiles,
-                                                               tileCount.p, 2));
+                launch_pdl(k_gather, (unsigned)(numTiles), kTileThreads, smemG, st, n, ctl, ws.perm.p, pin, dst, nMax, numTiles,
+                                                               tileCount.p, 2, SelfMap{});
             } else {
-                KL(k_gather<<<numTiles, kTileThreads, smemG, st>>>(n, ctl, ws.perm.p, pin, dst, nMax, numTiles,
-                                                               tileCount.p));
+                launch_pdl(k_gather, (unsigned)(numTiles), kTileThreads, smemG, st, n, ctl, ws.perm.p, pin, dst, nMax, numTiles,
+                                                               tileCount.p, 3, SelfMap{});
             }
             if (s == cfg.substeps - 1) rec(ev[7]);  // final storage order (overlapped download)
             launch_pdl(k_level_scan, (unsigned)(nMax + 1), 1024, 0, st, ctl, numTiles, tileCount.p, levelCount.p);
@@ -979,12 +979,12 @@ struct apbf_gpu_solver {
         rec(ev[5]);
         if (metrics) {
             // allDensities(x) over a throwaway grid (solver.hpp:271-279).
-            KL(k_grid_reset<<<1, 1, 0, st>>>(ctl, 1));
-            KL(k_aabb<<<blocks(n, kAabbBlock), kAabbBlock, 0, st>>>(n, set[cur].X.p, ctl, 1));
+            launch_pdl(k_grid_reset, (unsigned)(1), 1, 0, st, ctl, 1);
+            launch_pdl(k_aabb, (unsigned)(blocks(n, kAabbBlock)), kAabbBlock, 0, st, n, set[cur].X.p, ctl, 1);
             ws.run_grid(1, set[cur].X.p, n, cfg.h, cfg.h, false, radius);
-            KL(k_gather_posmass<<<blocks(n, 256), 256, 0, st>>>(n, ctl, ws.perm.p, set[cur].X.p,
-                                                             set[cur].XS.p, sortedPM.p));
-            KL(k_density_stats<<<blocks(n, 256), 256, 0, st>>>(n, ctl, sortedPM.p, ws.cellCount.p, sc.kc));
+            launch_pdl(k_gather_posmass, (unsigned)(blocks(n, 256)), 256, 0, st, n, ctl, ws.perm.p, set[cur].X.p,
+                                                             set[cur].XS.p, sortedPM.p);
+            launch_pdl(k_density_stats, (unsigned)(blocks(n, 256)), 256, 0, st, n, ctl, sortedPM.p, ws.cellCount.p, sc.kc);
             LAUNCH_CHECK();
         }
         rec(ev[6]);
@@ -1555,28 +1555,28 @@ struct apbf_gpu_solver {
         seg_begin(segLod);  // (buffers sized above: the recording allocates nothing)
         if (dtvs) {
             const CamFrame f = make_frame(cam);
-            KL(k_splat_prep<<<blocks((long long)px, 256), 256, 0, st>>>(f, ws.depth.p, ws.rays.p, ws.raysa.p));
-            KL(k_splat<<<blocks(nn, 256), 256, 0, st>>>(nn, X, radius, f, ws.depth.p, ws.rays.p, ws.raysa.p));
+            launch_pdl(k_splat_prep, (unsigned)(blocks((long long)px, 256)), 256, 0, st, f, ws.depth.p, ws.rays.p, ws.raysa.p);
+            launch_pdl(k_splat, (unsigned)(blocks(nn, 256)), 256, 0, st, nn, X, radius, f, ws.depth.p, ws.rays.p, ws.raysa.p);
             T.allreduce(ws.depth.p, px, RType::I32, ROp::Min, st);  // positive float bits: int order
-            KL(k_dtvs_gap<<<blocks(nn, 256), 256, 0, st>>>(nn, X, radius, f, ws.depth.p, ws.dist.p,
-                                                         ws.keys.p, ws.ctl.p));
+            launch_pdl(k_dtvs_gap, (unsigned)(blocks(nn, 256)), 256, 0, st, nn, X, radius, f, ws.depth.p, ws.dist.p,
+                                                         ws.keys.p, ws.ctl.p);
             T.allreduce(&ws.ctl.p->sample_count, 1, RType::I32, ROp::Sum, st);
         } else {
-            KL(k_dtc_dist<<<blocks(nn, 256), 256, 0, st>>>(nn, X, cam.eye[0], cam.eye[1], cam.eye[2],
-                                                         ws.dist.p, ws.keys.p));
+            launch_pdl(k_dtc_dist, (unsigned)(blocks(nn, 256)), 256, 0, st, nn, X, cam.eye[0], cam.eye[1], cam.eye[2],
+                                                         ws.dist.p, ws.keys.p);
         }
         if (lod.auto_range) {
-            KL(k_rs_init<<<1, 1024, 0, st>>>(ws.rs.p, ws.ctl.p, (int)nAll, dtvs ? 1 : 0));
+            launch_pdl(k_rs_init, (unsigned)(1), 1024, 0, st, ws.rs.p, ws.ctl.p, (int)nAll, dtvs ? 1 : 0);
             const int hb = std::min(blocks(nn, 256), 16 * 148);
             for (int pass = 0; pass < 3; ++pass) {
-                KL(k_rs_hist<<<hb, 256, 0, st>>>(nn, ws.keys.p, ws.rs.p, pass));
+                launch_pdl(k_rs_hist, (unsigned)(hb), 256, 0, st, nn, ws.keys.p, ws.rs.p, pass);
                 T.allreduce(&ws.rs.p->hist[0][0], 4 * 2048, RType::U32, ROp::Sum, st);
-                KL(k_rs_select<<<1, 1024, 0, st>>>(ws.rs.p, pass));
+                launch_pdl(k_rs_select, (unsigned)(1), 1024, 0, st, ws.rs.p, pass);
             }
         }
-        KL(k_lod_params<<<1, 1, 0, st>>>(ws.rs.p, ws.ctl.p, lod.auto_range, lod.d_min, lod.d_max, dtvs ? 1 : 0));
-        KL(k_lod_map<<<blocks(nn, 256), 256, 0, st>>>(nn, ws.ctl.p, ws.dist.p, ws.keys.p, dtvs ? 1 : 0,
-                                                     lod.n_min, lod.n_max, LV));
+        launch_pdl(k_lod_params, (unsigned)(1), 1, 0, st, ws.rs.p, ws.ctl.p, lod.auto_range, lod.d_min, lod.d_max, dtvs ? 1 : 0);
+        launch_pdl(k_lod_map, (unsigned)(blocks(nn, 256)), 256, 0, st, nn, ws.ctl.p, ws.dist.p, ws.keys.p, dtvs ? 1 : 0,
+                                                     lod.n_min, lod.n_max, LV);
         LAUNCH_CHECK();
         seg_end(segLod);
     }
@@ -1777,7 +1777,7 @@ struct apbf_gpu_solver {
         clsRecv = clsBuf.p + (size_t)G * kCls;
         CK(cudaEventRecord(ev[0], st));
         tmark("start");
-        KL(k_frame_begin<<<1, 1, 0, st>>>(ctl));
+        launch_pdl(k_frame_begin, (unsigned)(1), 1, 0, st, ctl);
         if (assign_lod) {
             if (cfg.mode == APBF_MODE_PBF) {
                 KL(k_fill_int<<<blocks(n, 256), 256, 0, st>>>(set[cur].LV.p, n, nMax));
@@ -1887,8 +1887,8 @@ struct apbf_gpu_solver {
                         self);
             const int tilesL = std::max(1, (nL + kTileSize - 1) / kTileSize);
             const int smemG = (nMax + 1) * (int)sizeof(int);
-            KL(k_gather<<<tilesL, kTileThreads, smemG, st>>>(nL, ctl, ws.perm.p, rec, dst, nMax, tilesL,
-                                                           tileCount.p, 3, self));
+            launch_pdl(k_gather, (unsigned)(tilesL), kTileThreads, smemG, st, nL, ctl, ws.perm.p, rec, dst, nMax, tilesL,
+                                                           tileCount.p, 3, self);
             const int nOwn = ownE - ownB;
             // iteration order over owned + layer-1 ghosts (lambda is computed
             // redundantly for the latter), outer ghosts never active.  With
@@ -2026,8 +2026,8 @@ struct apbf_gpu_solver {
         spanLo.ensure(kMaxRanks);
         spanHi.ensure(kMaxRanks);
         seg_begin(segMetPre);
-        KL(k_grid_reset<<<1, 1, 0, st>>>(ctl, 1));
-        KL(k_aabb<<<blocks(n, kAabbBlock), kAabbBlock, 0, st>>>(n, cs.X, ctl, 1));
+        launch_pdl(k_grid_reset, (unsigned)(1), 1, 0, st, ctl, 1);
+        launch_pdl(k_aabb, (unsigned)(blocks(n, kAabbBlock)), kAabbBlock, 0, st, n, cs.X, ctl, 1);
         KL(k_grid_reduce_pack<<<1, 1, 0, st>>>(ctl, 1, gridRed.p));
         T.allreduce(gridRed.p, 7, RType::I32, ROp::Min, st);
         KL(k_grid_reduce_unpack<<<1, 1, 0, st>>>(ctl, 1, gridRed.p));
@@ -2074,7 +2074,7 @@ struct apbf_gpu_solver {
         T.alltoallv(sp.data(), sb.data(), rp.data(), rb.data(), st);
         const int nm = (int)nM;
         ws.run_grid(1, recvPM.p, nm, cfg.h, cfg.h, false, radius, nullptr, nullptr, false);
-        KL(k_gather_posmass<<<blocks(nm, 256), 256, 0, st>>>(nm, ctl, ws.perm.p, recvPM.p, recvPM.p, sortedPM.p));
+        launch_pdl(k_gather_posmass, (unsigned)(blocks(nm, 256)), 256, 0, st, nm, ctl, ws.perm.p, recvPM.p, recvPM.p, sortedPM.p);
         KL(k_gather_int<<<blocks(nm, 256), 256, 0, st>>>(nm, ws.perm.p, ownedFlag.p, ownedSorted.p));
         KL(k_density_stats_owned<<<blocks(nm, 256), 256, 0, st>>>(nm, ctl, sortedPM.p, ownedSorted.p,
                                                                 ws.cellCount.p, make_kernel_consts(cfg.h)));
@@ -2502,9 +2502,9 @@ static void check_grid_args(int n, const float* pos, float h, float pad) {
 // Builds grid g on the uploaded tmp4 positions; returns host Ctl.
 static void component_grid(Workspace& ws, int g, int n, float h, float pad) {
     cudaStream_t st = ws.stream;
-    KL(k_frame_begin<<<1, 1, 0, st>>>(ws.ctl.p));
-    KL(k_grid_reset<<<1, 1, 0, st>>>(ws.ctl.p, g));
-    KL(k_aabb<<<blocks(n, kAabbBlock), kAabbBlock, 0, st>>>(n, ws.tmp4.p, ws.ctl.p, g));
+    launch_pdl(k_frame_begin, (unsigned)(1), 1, 0, st, ws.ctl.p);
+    launch_pdl(k_grid_reset, (unsigned)(1), 1, 0, st, ws.ctl.p, g);
+    launch_pdl(k_aabb, (unsigned)(blocks(n, kAabbBlock)), kAabbBlock, 0, st, n, ws.tmp4.p, ws.ctl.p, g);
     ws.run_grid(g, ws.tmp4.p, n, h, pad, false, 0.f);
     ws.read_ctl();
     if (ws.h_ctl->runtime_error) fail(APBF_ERR_RUNTIME, "grid cell count exceeds limit; domain blew up");
@@ -2564,15 +2564,15 @@ int32_t apbf_gpu_neighbor_lists(int32_t n, const float* positions, float h, floa
         iota.ensure(n);
         cnt.ensure((size_t)groups * 32);
         gbase.ensure(groups);
-        KL(k_gather_posmass<<<blocks(n, 256), 256, 0, st>>>(n, ws.ctl.p, ws.perm.p, ws.tmp4.p, ws.tmp4.p,
-                                                         sorted.p));
+        launch_pdl(k_gather_posmass, (unsigned)(blocks(n, 256)), 256, 0, st, n, ws.ctl.p, ws.perm.p, ws.tmp4.p, ws.tmp4.p,
+                                                         sorted.p);
         KL(k_iota<<<blocks(n, 256), 256, 0, st>>>(iota.p, n));
         long long cap = (long long)groups * 32 * 48;
         for (;;) {
             lists.release();
             lists.ensure((size_t)cap);
-            KL(k_frame_begin<<<1, 1, 0, st>>>(ws.ctl.p));
-            KL(k_list_reset<<<1, 1, 0, st>>>(ws.ctl.p));
+            launch_pdl(k_frame_begin, (unsigned)(1), 1, 0, st, ws.ctl.p);
+            launch_pdl(k_list_reset, (unsigned)(1), 1, 0, st, ws.ctl.p);
             KL(k_build_lists<<<blocks(n, kListThreads), kListThreads, 0, st>>>(
                 n, ws.ctl.p, iota.p, sorted.p, ws.cellCount.p, h, h * h, lists.p, cnt.p, gbase.p, cap));
             LAUNCH_CHECK();
@@ -2617,8 +2617,8 @@ int32_t apbf_gpu_all_densities(int32_t n, const float* positions, const float* m
         sorted.ensure(n);
         rho.ensure(n);
         cudaStream_t st = ws.stream;
-        KL(k_gather_posmass<<<blocks(n, 256), 256, 0, st>>>(n, ws.ctl.p, ws.perm.p, ws.tmp4.p, ws.tmp4.p,
-                                                         sorted.p));
+        launch_pdl(k_gather_posmass, (unsigned)(blocks(n, 256)), 256, 0, st, n, ws.ctl.p, ws.perm.p, ws.tmp4.p, ws.tmp4.p,
+                                                         sorted.p);
         KL(k_density_out<<<blocks(n, 256), 256, 0, st>>>(n, ws.ctl.p, sorted.p, ws.perm.p, ws.cellCount.p,
                                                       make_kernel_consts(h), rho.p));
         LAUNCH_CHECK();
@@ -2656,16 +2656,16 @@ int32_t apbf_gpu_vorticity(int32_t n, const float* positions, const float* veloc
         stage.ensure(3 * (size_t)n);
         CK(cudaMemcpyAsync(stage.p, velocities, sizeof(float) * 3 * n, cudaMemcpyHostToDevice, st));
         KL(k_unpack_x<<<blocks(n, 256), 256, 0, st>>>(n, stage.p, vin.p));
-        KL(k_gather_posmass<<<blocks(n, 256), 256, 0, st>>>(n, ws.ctl.p, ws.perm.p, ws.tmp4.p, ws.tmp4.p,
-                                                         sorted.p));
-        KL(k_gather_posmass<<<blocks(n, 256), 256, 0, st>>>(n, ws.ctl.p, ws.perm.p, vin.p, vin.p, vs.p));
+        launch_pdl(k_gather_posmass, (unsigned)(blocks(n, 256)), 256, 0, st, n, ws.ctl.p, ws.perm.p, ws.tmp4.p, ws.tmp4.p,
+                                                         sorted.p);
+        launch_pdl(k_gather_posmass, (unsigned)(blocks(n, 256)), 256, 0, st, n, ws.ctl.p, ws.perm.p, vin.p, vin.p, vs.p);
         KL(k_iota<<<blocks(n, 256), 256, 0, st>>>(iota.p, n));
         long long cap = (long long)groups * 32 * 48;
         for (;;) {
             lists.release();
             lists.ensure((size_t)cap);
-            KL(k_frame_begin<<<1, 1, 0, st>>>(ws.ctl.p));
-            KL(k_list_reset<<<1, 1, 0, st>>>(ws.ctl.p));
+            launch_pdl(k_frame_begin, (unsigned)(1), 1, 0, st, ws.ctl.p);
+            launch_pdl(k_list_reset, (unsigned)(1), 1, 0, st, ws.ctl.p);
             KL(k_build_lists<<<blocks(n, kListThreads), kListThreads, 0, st>>>(
                 n, ws.ctl.p, iota.p, sorted.p, ws.cellCount.p, h, h * h, lists.p, cnt.p, gbase.p, cap));
             LAUNCH_CHECK();
@@ -2704,7 +2704,7 @@ static void component_lod(int n, const float* positions, const apbf_camera* cam,
     upload_pos4(ws, n, positions);
     DBuf<int> lv;
     lv.ensure(n);
-    KL(k_frame_begin<<<1, 1, 0, ws.stream>>>(ws.ctl.p));
+    launch_pdl(k_frame_begin, (unsigned)(1), 1, 0, ws.stream, ws.ctl.p);
     run_lod(ws, ws.tmp4.p, n, *cam, *lod, radius, lv.p);
     CK(cudaMemcpyAsync(levels_out, lv.p, sizeof(int) * n, cudaMemcpyDeviceToHost, ws.stream));
     CK(cudaStreamSynchronize(ws.stream));
@@ -2739,11 +2739,11 @@ int32_t apbf_gpu_splat(int32_t n, const float* positions, float radius, const ap
         ws.depth.ensure(px);
         ws.rays.ensure(px);
         ws.raysa.ensure(px);
-        KL(k_splat_prep<<<blocks((long long)px, 256), 256, 0, ws.stream>>>(f, ws.depth.p, ws.rays.p, ws.raysa.p));
+        launch_pdl(k_splat_prep, (unsigned)(blocks((long long)px, 256)), 256, 0, ws.stream, f, ws.depth.p, ws.rays.p, ws.raysa.p);
         if (n > 0) {
             upload_pos4(ws, n, positions);
-            KL(k_splat<<<blocks(n, 256), 256, 0, ws.stream>>>(n, ws.tmp4.p, radius, f, ws.depth.p, ws.rays.p,
-                                                           ws.raysa.p));
+            launch_pdl(k_splat, (unsigned)(blocks(n, 256)), 256, 0, ws.stream, n, ws.tmp4.p, radius, f, ws.depth.p, ws.rays.p,
+                                                           ws.raysa.p);
         }
         LAUNCH_CHECK();
         CK(cudaMemcpyAsync(depth_out, ws.depth.p, sizeof(float) * px, cudaMemcpyDeviceToHost, ws.stream));
@@ -2785,7 +2785,7 @@ int32_t apbf_gpu_count_contacts(int32_t n, const float* positions, const apbf_sd
         Workspace& ws = component_ws();
         CK(cudaMemcpyAsync(ws.scene.p, &sc, sizeof(Scene), cudaMemcpyHostToDevice, ws.stream));
         upload_pos4(ws, n, positions);
-        KL(k_frame_begin<<<1, 1, 0, ws.stream>>>(ws.ctl.p));
+        launch_pdl(k_frame_begin, (unsigned)(1), 1, 0, ws.stream, ws.ctl.p);
         KL(k_count_contacts<<<blocks(n, 256), 256, 0, ws.stream>>>(n, ws.tmp4.p, ws.scene.p, radius, ws.ctl.p));
         LAUNCH_CHECK();
         ws.read_ctl();
