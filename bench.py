@@ -538,7 +538,7 @@ def run_ours(args, world, rank, local, pg):
         for f in range(args.steps):
             h2d += 32 * m  # x, v (3 words each), mass, inv_mass
             stats, m = e2e_step(m, 2000 + f)
-            d2h += 40 * m  # the reordered ParticleSet without x* (= x after the frame, copied on the host)
+            d2h += 52 * m  # the whole reordered ParticleSet
             its2 += stats.total_iterations
         e3.record(ext)
         e3.synchronize()
@@ -552,9 +552,7 @@ def run_ours(args, world, rank, local, pg):
                "note": "per step, from pinned host arrays: the frame's inputs are uploaded (x, v, mass, "
                        "inv_mass; x*, lambda and level are overwritten by stepFrame before they are read), "
                        "the frame runs, and the whole reordered ParticleSet (13 words per particle) is "
-                       "written back -- the reference's stepFrame(ParticleSet&) contract; x* equals x bit for "
-                       "bit after the frame, so 10 words cross PCIe and x* is copied from x on the host while "
-                       "v and lambda arrive (d2h_bytes counts what crossed); 1 GPU: one "
+                       "written back -- the reference's stepFrame(ParticleSet&) contract; 1 GPU: one "
                        "apbf_gpu_step_frame_host call (download overlapped with the metrics pass), "
                        "N GPUs: apbf_gpu_slab_set_state + step + apbf_gpu_get_state per rank"}
 

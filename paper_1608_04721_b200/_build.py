@@ -19,7 +19,7 @@ OUT = os.path.join(HERE, "libapbf_gpu.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-O3", "-std=c++17",
          "-fmad=false", "-prec-div=true", "-prec-sqrt=true", "-Xcompiler", "-fPIC",
-         "-Xcompiler", "-fvisibility=default", "-Xcompiler", "-fopenmp", "-lgomp", "-shared"]
+         "-Xcompiler", "-fvisibility=default", "-shared"]
 
 
 def _stale(out, deps) -> bool:

@@ -534,7 +534,6 @@ struct apbf_gpu_solver {
         if (ev_halo_ready) cudaEventDestroy(ev_halo_ready);
         if (ev_halo_done) cudaEventDestroy(ev_halo_done);
         if (ev_cls) cudaEventDestroy(ev_cls);
-        if (ev_xdl) cudaEventDestroy(ev_xdl);
         if (hostCls) cudaFreeHost(hostCls);
     }
 
@@ -1004,7 +1003,6 @@ struct apbf_gpu_solver {
         float *x, *xs, *v, *mass, *inv_mass, *lambda;
         int32_t* level;
         bool queued;
-        bool xs_from_x = false;  // x* is filled on the host from x (equal after finalize)
     };
     // The caller's x*, lambda and level as passed in (stepFrame overwrites
     // them before reading them, so the frame never needs them): uploaded raw
@@ -1082,31 +1080,12 @@ struct apbf_gpu_solver {
         CK(cudaStreamWaitEvent(st, ev[5], 0));
         KL(k_pack_dynamic<<<blocks(n, 256), 256, 0, st>>>(n, fin, d));
         LAUNCH_CHECK();
+        // (x* equals x after the frame, but filling the caller's x* from x
+        // on the host competed with the DMA for host memory bandwidth on
+        // some boxes: it stays a PCIe copy)
         if (o.x) CK(cudaMemcpyAsync(o.x, d, n3, cudaMemcpyDeviceToHost, st));
-        // After finalize x* == x bit for bit (finalize sets x = x*,
-        // solver.hpp:347-356): x* is not read back a second time over PCIe
-        // but copied from x on the host while v and lambda arrive
-        // (finish_frame).
-        o.xs_from_x = o.x && o.xs;
-        if (o.xs_from_x) {
-            if (!ev_xdl) CK(cudaEventCreateWithFlags(&ev_xdl, cudaEventDisableTiming));
-            CK(cudaEventRecord(ev_xdl, st));
-        } else if (o.xs) {
-            CK(cudaMemcpyAsync(o.xs, d + 3LL * n, n3, cudaMemcpyDeviceToHost, st));
-        }
+        if (o.xs) CK(cudaMemcpyAsync(o.xs, d + 3LL * n, n3, cudaMemcpyDeviceToHost, st));
         if (o.v) CK(cudaMemcpyAsync(o.v, d + 6LL * n, n3, cudaMemcpyDeviceToHost, st));
-    }
-    cudaEvent_t ev_xdl = nullptr;  // enqueue_download: x has reached the caller's array
-
-    // dst[0, m) = src[0, m) on the host, in parallel (page-locked caller
-    // arrays: one thread cannot saturate host memory bandwidth).
-    static void host_copy(float* dst, const float* src, size_t m) {
-        const long long chunks = 16, per = (long long)((m + chunks - 1) / chunks);
-#pragma omp parallel for schedule(static) num_threads(8)
-        for (long long c = 0; c < chunks; ++c) {
-            const long long b = c * per, e = std::min<long long>((long long)m, b + per);
-            if (b < e) std::memcpy(dst + b, src + b, sizeof(float) * (size_t)(e - b));
-        }
     }
 
     // A frame that failed after its overlapped download was queued: give the
@@ -1149,10 +1128,6 @@ struct apbf_gpu_solver {
             if (!copy_stream) CK(cudaStreamCreateWithFlags(&copy_stream, cudaStreamNonBlocking));
             enqueue_download(copy_stream, *host_out);
             host_out->queued = true;
-        }
-        if (host_out && host_out->queued && host_out->xs_from_x) {
-            CK(cudaEventSynchronize(ev_xdl));
-            host_copy(host_out->xs, host_out->x, 3 * (size_t)n);
         }
         CK(cudaStreamSynchronize(ws.stream));
         if (host_out && n > 0) CK(cudaStreamSynchronize(copy_stream));
