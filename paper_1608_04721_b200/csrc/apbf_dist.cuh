@@ -338,7 +338,7 @@ __global__ void k_unpack_recs(int cnt, const Rec* __restrict__ in, StateSet d, i
 
 // One all-reduce instead of three for the substep's grid: [~abort, lo(3),
 // ~hi(3)] all-reduced with MIN (bitwise not reverses the order of ordered
-// ints without overflow), then written back.
+// ints without overflow), then written back (k_grid_unpack_params).
 __global__ void k_grid_reduce_pack(const Ctl* ctl, int g, int* __restrict__ buf) {
     const GridDev& G = ctl->grid[g];
     buf[0] = ~ctl->abort;
@@ -347,13 +347,22 @@ __global__ void k_grid_reduce_pack(const Ctl* ctl, int g, int* __restrict__ buf)
         buf[4 + a] = ~G.hi_ord[a];
     }
 }
-__global__ void k_grid_reduce_unpack(Ctl* ctl, int g, const int* __restrict__ buf) {
+// The substep's grid after its all-reduce, in one launch: unpack, the grid
+// parameters (thread 0, k_grid_params), and the two per-substep counters the
+// next passes accumulate into cleared by the whole CTA (instead of two
+// memset nodes and two single-thread kernels).
+__global__ void k_grid_unpack_params(Ctl* ctl, int g, const int* __restrict__ buf, float h, float pad,
+                                     int* __restrict__ zeroA, int nA, int* __restrict__ zeroB, int nB) {
+    for (int t = threadIdx.x; t < nA; t += blockDim.x) zeroA[t] = 0;
+    for (int t = threadIdx.x; t < nB; t += blockDim.x) zeroB[t] = 0;
+    if (threadIdx.x != 0) return;
     GridDev& G = ctl->grid[g];
     ctl->abort = ~buf[0];
     for (int a = 0; a < 3; ++a) {
         G.lo_ord[a] = buf[1 + a];
         G.hi_ord[a] = ~buf[4 + a];
     }
+    grid_params(ctl, g, h, pad);
 }
 
 // K16 for the owned slice [b, b + m) of the sorted set, written to the front

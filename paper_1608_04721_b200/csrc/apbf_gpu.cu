@@ -1778,18 +1778,18 @@ struct apbf_gpu_solver {
             // everywhere; the abort flag travels alongside
             KL(k_grid_reduce_pack<<<1, 1, 0, st>>>(ctl, 0, gridRed.p));
             T.allreduce(gridRed.p, 7, RType::I32, ROp::Min, st);
-            KL(k_grid_reduce_unpack<<<1, 1, 0, st>>>(ctl, 0, gridRed.p));
-            launch_pdl(k_grid_params, (unsigned)(1), 1, 0, st, ctl, 0, cfg.h, cfg.h);
+            // (unpack + grid parameters, and the layer histogram and class
+            // counters cleared, in one launch)
+            KL(k_grid_unpack_params<<<1, 256, 0, st>>>(ctl, 0, gridRed.p, cfg.h, cfg.h, layerHist.p, layer_cap,
+                                                      clsSend, G * kCls));
             // slabs: equal-work split (sum of 1 + level per layer) of the
             // global histogram, computed on the device
-            CK(cudaMemsetAsync(layerHist.p, 0, sizeof(int) * layer_cap, st));
             KL(k_layer_hist<<<std::max(1, std::min(blocks(n, 256 * kHistItems), 148 * 8)), 256, 0, st>>>(n, src.XS, src.LV, ctl, 0, cfg.h, layerHist.p,
                                                           layer_cap));
             T.allreduce(layerHist.p, layer_cap, RType::I32, ROp::Sum, st);
             KL(k_slab_partition<<<1, 256, sizeof(int) * std::min(layer_cap, kPartSmem), st>>>(
                 layerHist.p, ctl, G, 2, zRange.p, layer_cap));
             // migration + halo in one all-to-all, previous global order kept
-            CK(cudaMemsetAsync(clsSend, 0, sizeof(int) * G * kCls, st));
             KL(k_dest_mask<<<std::max(1, std::min(blocks(n, 256), 148 * 4)), 256, 0, st>>>(n, src.XS, ctl, 0, cfg.h, zRange.p, zRange.p + G,
                                                          G, 2, destMask.p, clsSend));
             tmark("pre-exchange");
@@ -2005,14 +2005,13 @@ struct apbf_gpu_solver {
         launch_pdl(k_aabb, (unsigned)(blocks(n, kAabbBlock)), kAabbBlock, 0, st, n, cs.X, ctl, 1);
         KL(k_grid_reduce_pack<<<1, 1, 0, st>>>(ctl, 1, gridRed.p));
         T.allreduce(gridRed.p, 7, RType::I32, ROp::Min, st);
-        KL(k_grid_reduce_unpack<<<1, 1, 0, st>>>(ctl, 1, gridRed.p));
-        launch_pdl(k_grid_params, (unsigned)(1), 1, 0, st, ctl, 1, cfg.h, cfg.h);
+        KL(k_grid_unpack_params<<<1, 256, 0, st>>>(ctl, 1, gridRed.p, cfg.h, cfg.h, clsSend, G * kCls, nullptr,
+                                                  0));
         KL(k_span_init<<<1, 32, 0, st>>>(G, spanLo.p, spanHi.p));
         KL(k_layer_minmax<<<blocks(n, 256), 256, 0, st>>>(n, cs.X, ctl, 1, cfg.h, spanLo.p + g, spanHi.p + g));
         T.allreduce(spanLo.p, G, RType::I32, ROp::Min, st);
         T.allreduce(spanHi.p, G, RType::I32, ROp::Max, st);
         KL(k_metrics_ranges<<<1, 32, 0, st>>>(G, g, spanLo.p, spanHi.p));
-        CK(cudaMemsetAsync(clsSend, 0, sizeof(int) * G * kCls, st));
         KL(k_dest_mask<<<std::max(1, std::min(blocks(n, 256), 148 * 4)), 256, 0, st>>>(n, cs.X, ctl, 1, cfg.h, spanLo.p, spanHi.p, G, 1,
                                                      destMask.p, clsSend));
         exchange_classes_begin(T, 1);
